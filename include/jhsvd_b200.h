@@ -1,0 +1,106 @@
+/*
+ * jhsvd_b200.h -- C ABI of the B200-native blocked one-sided Jacobi (H)SVD.
+ *
+ * The reference (arxiv 1401.2720, package `jhsvd`) is pure Python whose
+ * arithmetic kernels are numba @njit functions; it has no C ABI.  The entry
+ * points below replace those kernels one for one (cited per function) plus
+ * the fused sweep driver.  A Python host binds them with ctypes
+ * (paper_1401_2720_b200/_lib.py); see INTEGRATION.md for the binding a
+ * reference maintainer would add.
+ *
+ * Conventions
+ *   - All matrices are FP64, column-major, DEVICE pointers owned by the
+ *     caller (PyTorch allocates them); `ld*` is the column stride in
+ *     elements.  Nothing here allocates device memory.
+ *   - `stream` is a cudaStream_t passed as void*; all work is enqueued on it
+ *     and nothing synchronizes, so results/counters are valid after the
+ *     stream is synchronized.
+ *   - Pivot tables are int32[steps][n/2][2], 0-based, in the reference's
+ *     order (strategy.make_strategy), resident on the device.
+ *   - Return value: 0 on success, -1000/-1001 for bad arguments/workspace,
+ *     otherwise the negated cudaError_t of the failed launch.
+ *   - Numeric failures are reported through device-side outputs (error key /
+ *     info / out[3]) exactly where the reference raises; the host maps them
+ *     to RankDeficiencyError / JDefinitenessError / UnsafeScalingError.
+ */
+#ifndef JHSVD_B200_H
+#define JHSVD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Device workspace for jh_block_sweep at order n and block width w. */
+int64_t jh_sweep_workspace_bytes(int64_t n, int w);
+
+/*
+ * p-steps [first_step, first_step + nsteps) of one block sweep of
+ * run_block_jacobi_inplace (reference driver.py:125-200, task :153-174):
+ * per task Gram (blockkernel.py:76-107), Cholesky (:110-145), inner
+ * pointwise Jacobi (:278-400), and -- when the task rotated -- the
+ * post-multiplication of [Gp Gq] and [Vp Vq] (:407-428).
+ *   G  m x n (ld ldg), V nv x n (ld ldv) or NULL; updated in place.
+ *   w  block width (shortened order), even, 2 <= w <= 64, n % w == 0.
+ *   counters: uint64[3] device: [0] += rotations, [1] += proper rotations,
+ *     [2] = min error key (initialise to UINT64_MAX); key layout
+ *     p-step<<38 | task<<16 | status<<13 | 1-based index, status 1 =
+ *     Cholesky pivot, 2 = zero column, 3 = hyperbolic domain.
+ */
+int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int64_t ldv,
+                   int64_t nv, int w, const int32_t *outer, int first_step, int nsteps,
+                   const int32_t *inner, int64_t n_plus, int inner_limit, double tol_c,
+                   void *workspace, int64_t ws_bytes, unsigned long long *counters,
+                   void *stream);
+
+/* gram (blockkernel.py:99-107): H = A^T A, A m x c. */
+int jh_gram(const double *A, int64_t lda, int64_t m, int c, double *H, void *stream);
+
+/* cholesky_in_place (blockkernel.py:130-145): H (c x c) overwritten with L,
+ * R = L^T; *info (device int) = 0 or the 1-based bad pivot. */
+int jh_cholesky(double *H, int c, double *R, int *info, void *stream);
+
+/* inner_jacobi (blockkernel.py:346-400) on one c x c factor, c even <= 64.
+ * R in place, V = accumulated transformation; out (device int64[5]) =
+ * rotations, proper, sweeps, status (0 ok, 2 zero column, 3 hyperbolic
+ * domain), 1-based bad column. */
+int jh_inner_jacobi(double *R, double *V, int c, const int32_t *steps, const int8_t *signs,
+                    double tol_c, int max_sweeps, int64_t *out, void *stream);
+
+/* postmultiply (blockkernel.py:420-428): C = A B, per-entry in-order fma
+ * chains over k; A m x k, B k x n2, C m x n2 (C must not alias A or B). */
+int jh_gemm(const double *A, int64_t lda, int64_t m, int k, const double *B, int64_t ldb,
+            int n2, double *C, int64_t ldc, void *stream);
+
+/* solve_for_v back substitution (driver.py:203-211): R out = W. */
+int jh_back_substitute(const double *R, int n, const double *W, int nc, double *out,
+                       void *stream);
+
+/* robustnorm.safe_bounds (robustnorm.py:90-113), host function. */
+void jh_safe_bounds(int64_t n, double *mu_tilde, double *nu_hat);
+
+/* robustnorm.norm2 per column (robustnorm.py:295-334): ||G[:, i]|| =
+ * s[i] / 2**js[i]; js, s device arrays of length n. */
+int jh_column_norms(const double *G, int64_t ldg, int64_t m, int64_t n, int64_t *js, double *s,
+                    void *stream);
+
+/* check_column_scaling (driver.py:99-112): *bad (device, init UINT64_MAX)
+ * = smallest 1-based column with norm outside [mu_tilde, sqrt(nu_hat)]. */
+int jh_check_scaling(const double *G, int64_t ldg, int64_t m, int64_t n,
+                     unsigned long long *bad, void *stream);
+
+/* extract_sigma + U = G / sigma (driver.py:230-238, 294-297); *bad (device,
+ * init UINT64_MAX) = smallest 1-based zero column. */
+int jh_sigma_u(const double *G, int64_t ldg, int64_t m, int64_t n, double *sigma, double *U,
+               int64_t ldu, unsigned long long *bad, void *stream);
+
+/* Diagnostic: DMMA (mma.sync m8n8k4 f64) vs in-order fma chain. */
+int jh_probe_dmma(const double *A, const double *B, const double *C, double *Dm, double *Df,
+                  int ntests, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* JHSVD_B200_H */

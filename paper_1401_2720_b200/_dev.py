@@ -1,0 +1,53 @@
+"""Device-buffer helpers: column-major FP64 matrices held in PyTorch.
+
+An m x n matrix lives on the device as a contiguous torch tensor of shape
+(n, m) -- row c is column c -- i.e. column-major storage, the layout the
+reference (and the paper) uses.  Host numpy arrays come
+in and go out in Fortran order, like the reference's.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+
+def device() -> torch.device:
+    from . import _lib
+
+    _lib.require_cuda()  # loud NativeUnavailable without a B200 / the library
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def is_torch(a) -> bool:
+    return isinstance(a, torch.Tensor)
+
+
+def to_colmajor(a, copy: bool = False) -> torch.Tensor:
+    """m x n host or device matrix -> (n, m) contiguous FP64 device tensor."""
+    if is_torch(a):
+        t = a.to(device=device(), dtype=torch.float64)
+        if t.ndim != 2:
+            raise ValueError("expected a 2-d matrix")
+        st = t.t()
+        if st.is_contiguous() and not copy and st.data_ptr() == a.data_ptr():
+            return st
+        return st.contiguous() if not copy else st.contiguous().clone()
+    arr = np.asarray(a, dtype=np.float64)
+    if arr.ndim != 2:
+        raise ValueError("expected a 2-d matrix")
+    host = torch.from_numpy(np.ascontiguousarray(arr.T))
+    if host.numel() >= (1 << 20):
+        host = host.pin_memory()
+    return host.to(device(), non_blocking=True)
+
+
+def from_colmajor(t: torch.Tensor, as_numpy: bool):
+    """(n, m) column-major storage -> m x n result (numpy F-order or torch view)."""
+    if not as_numpy:
+        return t.t()
+    return np.asfortranarray(t.cpu().numpy().T)
+
+
+def vector_out(t: torch.Tensor, as_numpy: bool):
+    return t.cpu().numpy() if as_numpy else t

@@ -1,0 +1,45 @@
+// Diagnostic probe: rounding semantics of the FP64 tensor-core MMA
+// (mma.sync m8n8k4 f64, SASS DMMA) against an in-order fma chain over k.
+// If DMMA rounds after every k term in ascending order, the Gram and update
+// contractions can run on DMMA tiles and stay bitwise equal to the reference
+// (hard part H1).  Used by tests/ and the probe script;
+// not on the solver path.
+#include "jh_common.cuh"
+
+namespace jh {
+
+// test t: A 8x4 row-major, B 4x8 row-major, C 8x8 row-major.
+__global__ void k_probe_dmma(const double *__restrict__ A, const double *__restrict__ B,
+                             const double *__restrict__ C, double *__restrict__ Dm,
+                             double *__restrict__ Df, int ntests) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= ntests) return;
+  const double *a = A + warp * 32, *b = B + warp * 32, *c = C + warp * 64;
+  const int g = lane >> 2, tq = lane & 3;
+  const double ra = a[g * 4 + tq];
+  const double rb = b[tq * 8 + g];
+  const double c0 = c[g * 8 + 2 * tq], c1 = c[g * 8 + 2 * tq + 1];
+  double d0, d1;
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};\n"
+               : "=d"(d0), "=d"(d1)
+               : "d"(ra), "d"(rb), "d"(c0), "d"(c1));
+  Dm[warp * 64 + g * 8 + 2 * tq] = d0;
+  Dm[warp * 64 + g * 8 + 2 * tq + 1] = d1;
+  for (int j = 0; j < 2; j++) {
+    const int col = 2 * tq + j;
+    double acc = c[g * 8 + col];
+    for (int k = 0; k < 4; k++) acc = fma(a[g * 4 + k], b[k * 8 + col], acc);
+    Df[warp * 64 + g * 8 + col] = acc;
+  }
+}
+
+}  // namespace jh
+
+extern "C" int jh_probe_dmma(const double *A, const double *B, const double *C, double *Dm,
+                             double *Df, int ntests, void *stream) {
+  const int threads = 256;
+  const int blocks = (ntests * 32 + threads - 1) / threads;
+  jh::k_probe_dmma<<<blocks, threads, 0, (cudaStream_t)stream>>>(A, B, C, Dm, Df, ntests);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : -(int)e;
+}

@@ -1,0 +1,516 @@
+// The p-step of the blocked one-sided Jacobi (H)SVD on one B200.
+//
+// Reference: run_block_jacobi_inplace / task (pkg/src/jhsvd/driver.py:125-200)
+// with the block-pair kernels of pkg/src/jhsvd/blockkernel.py.  One p-step is
+// b/2 independent tasks, task t pairing block-columns (p, q) of width bw = w/2:
+//
+//   K1 gram      H = [Gp Gq]^T [Gp Gq]           (blockkernel.py:76-107)
+//   K2 factor    H = L L^T, R = L^T              (blockkernel.py:110-145)
+//   K2 inner     pointwise Jacobi on R -> V'     (blockkernel.py:278-400)
+//   K3 update    [Gp Gq] <- [Gp Gq] V', [Vp Vq] <- [Vp Vq] V'  if rotations
+//                                                (blockkernel.py:407-428,
+//                                                 driver.py:165-173)
+//
+// Layout in HBM: G is m x n column-major (column c at G + c*ldg), V is nv x n
+// column-major; block-column p is the contiguous range of bw columns
+// starting at p*bw.  Per-task scratch (H, V', rotation counts) is a small
+// workspace that stays L2-resident.
+#include "jh_common.cuh"
+
+#include <cstdio>
+
+namespace jh {
+
+constexpr int kMaxW = 64;          // largest block width the fused kernels take
+constexpr int kGramThreads = 256;
+constexpr int kGramChunk = 64;     // rows staged per smem chunk
+constexpr int kGramMaxEnt = (kMaxW * (kMaxW + 1) / 2 + kGramThreads - 1) / kGramThreads;
+constexpr int kUpdRows = 128;      // rows per update CTA
+constexpr int kUpdThreads = 256;
+
+struct Workspace {
+  double *H;      // [ntask][w][w]
+  double *Vacc;   // [ntask][w][w]
+  int64_t *rot;   // [ntask] rotations of the task in this p-step
+};
+
+__device__ __forceinline__ const double *pair_col(const double *base, int64_t ld, int p, int q,
+                                                  int bw, int j) {
+  const int64_t col = j < bw ? (int64_t)p * bw + j : (int64_t)q * bw + (j - bw);
+  return base + col * ld;
+}
+
+// ---------------------------------------------------------------------------
+// K1: Gram matrix of the block-column pair.  Every entry h[x][y] (x >= y) is
+// one fma chain over the m rows in ascending order starting from +0.0,
+// exactly _gram_kernel's; rows are staged through shared memory in chunks
+// (chunking does not reorder a chain).  Lower triangle mirrored.
+__global__ void __launch_bounds__(kGramThreads)
+k_gram(const double *__restrict__ G, int64_t ldg, int64_t m, const int32_t *__restrict__ pairs,
+       int bw, double *__restrict__ Hbuf) {
+  const int w = 2 * bw;
+  const int task = blockIdx.x;
+  const int p = pairs[2 * task], q = pairs[2 * task + 1];
+  extern __shared__ double sm[];
+  double *T = sm;  // [kGramChunk][w] row-major chunk
+  const int ne = w * (w + 1) / 2;
+  int ex[kGramMaxEnt], ey[kGramMaxEnt];
+  double acc[kGramMaxEnt];
+  int nmine = 0;
+  for (int e = threadIdx.x; e < ne; e += blockDim.x) {
+    // triangular index -> (x, y) with x >= y, column by column
+    int y = 0, rem = e;
+    while (rem >= w - y) {
+      rem -= w - y;
+      y++;
+    }
+    ex[nmine] = y + rem;
+    ey[nmine] = y;
+    acc[nmine] = 0.0;
+    nmine++;
+  }
+  for (int64_t c0 = 0; c0 < m; c0 += kGramChunk) {
+    const int nr = (int)min64(kGramChunk, m - c0);
+    for (int idx = threadIdx.x; idx < nr * w; idx += blockDim.x) {
+      const int i = idx % nr, x = idx / nr;
+      T[i * w + x] = pair_col(G, ldg, p, q, bw, x)[c0 + i];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kGramMaxEnt; k++) {
+      if (k < nmine) {
+        const int x = ex[k], y = ey[k];
+        double a = acc[k];
+        for (int i = 0; i < nr; i++) a = fma(T[i * w + x], T[i * w + y], a);
+        acc[k] = a;
+      }
+    }
+    __syncthreads();
+  }
+  double *H = Hbuf + (int64_t)task * w * w;
+#pragma unroll
+  for (int k = 0; k < kGramMaxEnt; k++) {
+    if (k < nmine) {
+      H[ey[k] * w + ex[k]] = acc[k];  // h[x, y]
+      H[ex[k] * w + ey[k]] = acc[k];  // h[y, x]
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2 building blocks, executed by one CTA of 32*max(1, w/2) threads.
+
+// Forward-looking Cholesky of the w x w matrix in smem (column-major, ld w),
+// lower triangle, _cholesky_kernel order.  Returns 0 or the 1-based pivot.
+__device__ int cta_cholesky(double *H, int w, int *s_status) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int k = 0; k < w; k++) {
+    if (tid == 0) {
+      const double d = H[k * w + k];
+      if (!(d > 0.0) || !isfinite(d))
+        *s_status = k + 1;
+      else
+        H[k * w + k] = sqrt(d);
+    }
+    __syncthreads();
+    if (*s_status) return *s_status;
+    const double l = H[k * w + k];
+    for (int x = k + 1 + tid; x < w; x += nt) H[k * w + x] = H[k * w + x] / l;
+    __syncthreads();
+    // trailing update: h[x][j] = fma(-h[x][k], h[j][k], h[x][j]) for k < j <= x
+    const int r = w - k - 1;
+    const int nupd = r * (r + 1) / 2;
+    for (int e = tid; e < nupd; e += nt) {
+      int jj = 0, rem = e;
+      while (rem >= r - jj) {
+        rem -= r - jj;
+        jj++;
+      }
+      const int j = k + 1 + jj, x = j + rem;
+      H[j * w + x] = fma(-H[k * w + x], H[k * w + j], H[j * w + x]);
+    }
+    __syncthreads();
+  }
+  return 0;
+}
+
+// Sweep loop of the pointwise one-sided Jacobi on R (w x w, smem col-major)
+// accumulating V (smem, starts at I); _inner_jacobi_kernel order
+// (blockkernel.py:278-334).  Warp pi owns pair pi of each inner p-step: its
+// lane 0 forms the three dot products as in-order fma chains and the
+// rotation parameters; all lanes apply the rotation (and the sorting swap)
+// to their rows.  Pairs of one p-step touch disjoint columns, so a single
+// CTA barrier per p-step orders everything.  On failure returns the status
+// of the first failing pair in reference order (smallest pair index in the
+// first failing p-step) with its 1-based local column.
+struct InnerOut {
+  int64_t rot, proper;
+  int sweeps, status, bad;
+};
+
+struct InnerShared {
+  int cnt[kMaxW];        // per warp: applied, proper (this sweep)
+  int fail[kMaxW / 2];   // per warp: (status << 16) | bad
+  int fail_min;          // smallest failing pair index in the current step
+};
+
+__device__ InnerOut cta_inner_jacobi(double *R, double *V, int w, const int32_t *__restrict__ steps,
+                                     const int8_t *sg, double tol_c, int max_sweeps,
+                                     InnerShared *sh) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int half = w / 2;
+  InnerOut out{0, 0, 0, 0, -1};
+  if (threadIdx.x == 0) sh->fail_min = 0x7fffffff;
+  __syncthreads();
+  for (int sw = 0; sw < max_sweeps; sw++) {
+    int a_r = 0, b_r = 0;
+    for (int si = 0; si < w - 1; si++) {
+      const int p = steps[(si * half + warp) * 2];
+      const int q = steps[(si * half + warp) * 2 + 1];
+      double cs = 1.0, tn = 0.0;
+      int act = 0;  // 0 skip, 1 rotate, 2 rotate + swap, -1 failure
+      int hyp = 0;
+      if (lane == 0) {
+        const double *cp = R + p * w, *cq = R + q * w;
+        double hpp = 0.0, hqq = 0.0, hpq = 0.0;
+        for (int i = 0; i < w; i++) {
+          const double gp = cp[i], gq = cq[i];
+          hpp = fma(gp, gp, hpp);
+          hqq = fma(gq, gq, hqq);
+          hpq = fma(gp, gq, hpq);
+        }
+        int st = 0, bad = 0;
+        if (hpp == 0.0) {
+          st = kZeroColumn;
+          bad = p + 1;
+        } else if (hqq == 0.0) {
+          st = kZeroColumn;
+          bad = q + 1;
+        } else if (!(fabs(hpq) < tol_c * sqrt(hpp) * sqrt(hqq))) {
+          hyp = (sg[p] > 0 && sg[q] < 0) ? 1 : 0;
+          const double t = hyp ? -1.0 : 1.0;
+          if (!rotation_core(hpp, hqq, hpq, t, cs, tn)) {
+            st = kHypDomain;
+            bad = p + 1;
+          } else {
+            a_r++;
+            if (cs != 1.0) b_r++;
+            act = 1;
+            if (!hyp) {
+              const double h1 = fma(-tn, hpq, hpp);
+              const double h2 = fma(tn, hpq, hqq);
+              if ((sg[p] > 0 && h1 < h2) || (sg[p] < 0 && h1 > h2)) act = 2;
+            }
+          }
+        }
+        if (st) {
+          act = -1;
+          sh->fail[warp] = (st << 16) | bad;
+          atomicMin(&sh->fail_min, warp);
+        }
+      }
+      act = __shfl_sync(0xffffffffu, act, 0);
+      if (act > 0) {
+        cs = __shfl_sync(0xffffffffu, cs, 0);
+        tn = __shfl_sync(0xffffffffu, tn, 0);
+        hyp = __shfl_sync(0xffffffffu, hyp, 0);
+        const double s = hyp ? tn : -tn;
+        const bool scale = cs != 1.0;
+        for (int i = lane; i < w; i += 32) {
+          double *rp = R + p * w + i, *rq = R + q * w + i;
+          double *vp = V + p * w + i, *vq = V + q * w + i;
+          const double gp = *rp, gq = *rq, xp = *vp, xq = *vq;
+          double np = fma(s, gq, gp), nq = fma(tn, gp, gq);
+          double mp = fma(s, xq, xp), mq = fma(tn, xp, xq);
+          if (scale) {
+            np = np * cs;
+            nq = nq * cs;
+            mp = mp * cs;
+            mq = mq * cs;
+          }
+          if (act == 2) {  // _swap_columns after the rotation
+            *rp = nq;
+            *rq = np;
+            *vp = mq;
+            *vq = mp;
+          } else {
+            *rp = np;
+            *rq = nq;
+            *vp = mp;
+            *vq = mq;
+          }
+        }
+      }
+      __syncthreads();
+      if (sh->fail_min != 0x7fffffff) {
+        const int f = sh->fail[sh->fail_min];
+        out.status = f >> 16;
+        out.bad = f & 0xffff;
+        out.sweeps = sw;
+        return out;
+      }
+    }
+    // sweep end: totals of applied / proper rotations over all warps
+    if (lane == 0) {
+      sh->cnt[2 * warp] = a_r;
+      sh->cnt[2 * warp + 1] = b_r;
+    }
+    __syncthreads();
+    int64_t ta = 0, tb = 0;
+    for (int k = 0; k < half; k++) {
+      ta += sh->cnt[2 * k];
+      tb += sh->cnt[2 * k + 1];
+    }
+    __syncthreads();
+    out.sweeps++;
+    out.rot += ta;
+    out.proper += tb;
+    if (ta == 0) break;
+  }
+  return out;
+}
+
+// K2: Cholesky + inner Jacobi for every task of the p-step; one CTA of
+// 32 * max(1, w/2) threads per task.  Dynamic smem: H/R and V (2 w^2 doubles).
+//   counters[0] += rotations, counters[1] += proper rotations,
+//   counters[2] = min error key (ULLONG_MAX when clean)
+__global__ void k_factor_inner(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
+                               int64_t *__restrict__ task_rot, const int32_t *__restrict__ pairs,
+                               int bw, int64_t n_plus, const int32_t *__restrict__ inner,
+                               int inner_limit, double tol_c, unsigned long long *counters,
+                               int pstep) {
+  const int w = 2 * bw;
+  const int task = blockIdx.x;
+  const int p = pairs[2 * task], q = pairs[2 * task + 1];
+  extern __shared__ double sm[];
+  double *H = sm;           // H, then R in place
+  double *V = sm + w * w;
+  __shared__ int8_t sg[kMaxW];
+  __shared__ InnerShared sh;
+  __shared__ int s_status;
+  const double *Hg = Hbuf + (int64_t)task * w * w;
+  for (int i = threadIdx.x; i < w * w; i += blockDim.x) {
+    H[i] = Hg[i];
+    V[i] = (i % w == i / w) ? 1.0 : 0.0;
+  }
+  for (int j = threadIdx.x; j < w; j += blockDim.x) {
+    const int64_t gcol = (j < bw ? (int64_t)p * bw + j : (int64_t)q * bw + (j - bw)) + 1;
+    sg[j] = gcol <= n_plus ? 1 : -1;
+  }
+  if (threadIdx.x == 0) s_status = 0;
+  __syncthreads();
+  const int info = cta_cholesky(H, w, &s_status);
+  if (info) {
+    if (threadIdx.x == 0) {
+      task_rot[task] = 0;
+      atomicMin(&counters[2], err_key(pstep, task, kCholesky, info));
+    }
+    return;
+  }
+  // R = L^T in place: upper <- lower transposed, strict lower <- 0
+  for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
+    const int i = e % w, j = e / w;
+    if (i < j) {
+      H[j * w + i] = H[i * w + j];
+      H[i * w + j] = 0.0;
+    }
+  }
+  __syncthreads();
+  const InnerOut o = cta_inner_jacobi(H, V, w, inner, sg, tol_c, inner_limit, &sh);
+  if (o.status) {
+    if (threadIdx.x == 0) {
+      task_rot[task] = 0;
+      atomicMin(&counters[2], err_key(pstep, task, o.status, o.bad));
+    }
+    return;
+  }
+  double *Vg = Vbuf + (int64_t)task * w * w;
+  for (int i = threadIdx.x; i < w * w; i += blockDim.x) Vg[i] = V[i];
+  if (threadIdx.x == 0) {
+    task_rot[task] = o.rot;
+    atomicAdd(&counters[0], (unsigned long long)o.rot);
+    atomicAdd(&counters[1], (unsigned long long)o.proper);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: post-multiplication of the tall pair columns by V' (in place), for G
+// rows (blockIdx.y < nbg) and V rows.  out[i][j] is one fma chain over k in
+// ascending order starting from +0.0 (_postmultiply_kernel).  Skipped for a
+// task without rotations (driver.py:165).
+__global__ void __launch_bounds__(kUpdThreads)
+k_update(double *__restrict__ G, int64_t ldg, int64_t m, double *__restrict__ Vm, int64_t ldv,
+         int64_t nv, const int32_t *__restrict__ pairs, int bw, const double *__restrict__ Vbuf,
+         const int64_t *__restrict__ task_rot, int nbg) {
+  const int w = 2 * bw;
+  const int task = blockIdx.x;
+  if (task_rot[task] == 0) return;
+  const int p = pairs[2 * task], q = pairs[2 * task + 1];
+  double *A;
+  int64_t ld, rows, r0;
+  if ((int)blockIdx.y < nbg) {
+    A = G;
+    ld = ldg;
+    rows = m;
+    r0 = (int64_t)blockIdx.y * kUpdRows;
+  } else {
+    A = Vm;
+    ld = ldv;
+    rows = nv;
+    r0 = (int64_t)(blockIdx.y - nbg) * kUpdRows;
+  }
+  if (r0 >= rows) return;
+  const int nr = (int)min64(kUpdRows, rows - r0);
+  extern __shared__ double sm[];
+  double *Vs = sm;                // [w][w] col-major: Vs[j*w + k] = v'[k][j]
+  double *As = sm + w * w;        // [w][kUpdRows]: As[k*kUpdRows + i]
+  const double *Vg = Vbuf + (int64_t)task * w * w;
+  for (int i = threadIdx.x; i < w * w; i += blockDim.x) Vs[i] = Vg[i];
+  for (int idx = threadIdx.x; idx < nr * w; idx += blockDim.x) {
+    const int i = idx % nr, k = idx / nr;
+    As[k * kUpdRows + i] = pair_col(A, ld, p, q, bw, k)[r0 + i];
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < nr * w; idx += blockDim.x) {
+    const int i = idx % nr, j = idx / nr;
+    double acc = 0.0;
+    for (int k = 0; k < w; k++) acc = fma(As[k * kUpdRows + i], Vs[j * w + k], acc);
+    const_cast<double *>(pair_col(A, ld, p, q, bw, j))[r0 + i] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Kernel-level entry points (blockkernel.cholesky_in_place / inner_jacobi).
+
+// Cholesky of one c x c matrix in global memory (any c), then R = L^T.
+__global__ void __launch_bounds__(1024)
+k_cholesky_single(double *__restrict__ H, int c, double *__restrict__ R, int *info) {
+  __shared__ int s_status;
+  if (threadIdx.x == 0) s_status = 0;
+  __syncthreads();
+  const int st = cta_cholesky(H, c, &s_status);
+  if (threadIdx.x == 0) *info = st;
+  if (st) return;
+  for (int64_t e = threadIdx.x; e < (int64_t)c * c; e += blockDim.x) {
+    const int i = (int)(e % c), j = (int)(e / c);
+    R[(int64_t)j * c + i] = (i <= j) ? H[(int64_t)i * c + j] : 0.0;
+  }
+}
+
+// Inner Jacobi of one c x c factor (c even, <= kMaxW).  R updated in place,
+// V receives the accumulated transformation.  out: rotations, proper,
+// sweeps, status, bad (1-based).
+__global__ void k_inner_single(double *__restrict__ R, double *__restrict__ V, int c,
+                               const int32_t *__restrict__ steps, const int8_t *__restrict__ signs,
+                               double tol_c, int max_sweeps, int64_t *out) {
+  extern __shared__ double sm[];
+  double *Rs = sm, *Vs = sm + c * c;
+  __shared__ int8_t sg[kMaxW];
+  __shared__ InnerShared sh;
+  for (int i = threadIdx.x; i < c * c; i += blockDim.x) {
+    Rs[i] = R[i];
+    Vs[i] = (i % c == i / c) ? 1.0 : 0.0;
+  }
+  for (int j = threadIdx.x; j < c; j += blockDim.x) sg[j] = signs[j];
+  __syncthreads();
+  const InnerOut o = cta_inner_jacobi(Rs, Vs, c, steps, sg, tol_c, max_sweeps, &sh);
+  for (int i = threadIdx.x; i < c * c; i += blockDim.x) {
+    R[i] = Rs[i];
+    V[i] = Vs[i];
+  }
+  if (threadIdx.x == 0) {
+    out[0] = o.rot;
+    out[1] = o.proper;
+    out[2] = o.sweeps;
+    out[3] = o.status;
+    out[4] = o.bad;
+  }
+}
+
+}  // namespace jh
+
+using namespace jh;
+
+extern "C" {
+
+// Bytes of device workspace jh_block_sweep needs for order n and width w.
+int64_t jh_sweep_workspace_bytes(int64_t n, int w) {
+  const int64_t ntask = n / w;  // b/2 with b = n / (w/2)
+  return ntask * (int64_t)w * w * 8 * 2 + ntask * 8 + 256;
+}
+
+// One block sweep (or p-steps [first_step, first_step + nsteps) of it) of
+// run_block_jacobi_inplace (driver.py:180-190) on device data.
+//   G: m x n (ld ldg), V: nv x n (ld ldv) or NULL, both updated in place.
+//   outer: int32[b-1][b/2][2] 0-based block indices (device),
+//   inner: int32[w-1][w/2][2] 0-based column indices (device).
+//   counters (device, uint64[3]): += rotations, += proper, min error key.
+// Returns 0, or a negative CUDA error code.
+int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int64_t ldv,
+                   int64_t nv, int w, const int32_t *outer, int first_step, int nsteps,
+                   const int32_t *inner, int64_t n_plus, int inner_limit, double tol_c,
+                   void *workspace, int64_t ws_bytes, unsigned long long *counters,
+                   void *stream) {
+  if (w < 2 || w % 2 || w > kMaxW || n % w) return -1000;
+  if (ws_bytes < jh_sweep_workspace_bytes(n, w)) return -1001;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int bw = w / 2;
+  const int ntask = (int)(n / w);
+  char *ws = (char *)workspace;
+  double *Hbuf = (double *)ws;
+  double *Vbuf = Hbuf + (int64_t)ntask * w * w;
+  int64_t *trot = (int64_t *)(Vbuf + (int64_t)ntask * w * w);
+  const int thr_inner = 32 * (bw > 1 ? bw : 1);
+  const int nbg = (int)cdiv(m, kUpdRows);
+  const int nbv = V ? (int)cdiv(nv, kUpdRows) : 0;
+  const size_t smem_gram = sizeof(double) * kGramChunk * w;
+  const size_t smem_inner = sizeof(double) * 2 * (size_t)w * w;
+  const size_t smem_upd = sizeof(double) * ((size_t)w * w + (size_t)w * kUpdRows);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(double) * (kMaxW * kMaxW + kMaxW * kUpdRows)));
+    cudaFuncSetAttribute(k_factor_inner, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(double) * 2 * kMaxW * kMaxW));
+    attr_set = true;
+  }
+  for (int s = first_step; s < first_step + nsteps; s++) {
+    const int32_t *pairs = outer + (int64_t)s * ntask * 2;
+    k_gram<<<ntask, kGramThreads, smem_gram, st>>>(G, ldg, m, pairs, bw, Hbuf);
+    k_factor_inner<<<ntask, thr_inner, smem_inner, st>>>(Hbuf, Vbuf, trot, pairs, bw, n_plus, inner,
+                                                 inner_limit, tol_c, counters, s);
+    dim3 grid(ntask, nbg + nbv);
+    k_update<<<grid, kUpdThreads, smem_upd, st>>>(G, ldg, m, V, ldv, nv, pairs, bw, Vbuf, trot,
+                                                  nbg);
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : -(int)e;
+}
+
+// cholesky_in_place (blockkernel.py:130-145): factors H (c x c, device,
+// overwritten) and writes R = L^T (zero strict lower) to R; *info (device)
+// = 0 or the 1-based bad pivot.
+int jh_cholesky(double *H, int c, double *R, int *info, void *stream) {
+  k_cholesky_single<<<1, 1024, 0, (cudaStream_t)stream>>>(H, c, R, info);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : -(int)e;
+}
+
+// inner_jacobi (blockkernel.py:346-400) on one c x c factor, c even <= 64.
+int jh_inner_jacobi(double *R, double *V, int c, const int32_t *steps, const int8_t *signs,
+                    double tol_c, int max_sweeps, int64_t *out, void *stream) {
+  if (c < 2 || c % 2 || c > kMaxW) return -1000;
+  const size_t smem = sizeof(double) * 2 * (size_t)c * c;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_inner_single, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(double) * 2 * kMaxW * kMaxW));
+    attr = true;
+  }
+  k_inner_single<<<1, 32 * (c / 2), smem, (cudaStream_t)stream>>>(R, V, c, steps, signs, tol_c,
+                                                                  max_sweeps, out);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : -(int)e;
+}
+
+}  // extern "C"

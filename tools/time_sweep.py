@@ -1,0 +1,47 @@
+"""Time block sweeps of the single-GPU engine on random input (dev tool).
+
+    python tools/time_sweep.py N [W] [SWEEPS] [STEPS]
+"""
+import sys
+import time
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_1401_2720_b200.driver import SolverConfig, SweepEngine  # noqa: E402
+from paper_1401_2720_b200.strategy import make_strategy  # noqa: E402
+
+
+def main():
+    n = int(sys.argv[1])
+    w = int(sys.argv[2]) if len(sys.argv) > 2 else 32
+    sweeps = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+    steps = int(sys.argv[4]) if len(sys.argv) > 4 else None
+    cfg = SolverConfig(block_width=w)
+    t0 = time.time()
+    outer = make_strategy("rrow", n // (w // 2))
+    inner = make_strategy("rrow", w)
+    print(f"strategy {time.time() - t0:.2f}s", flush=True)
+    eng = SweepEngine(n, n, n, cfg, outer, inner, n)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    G = torch.randn(n, n, dtype=torch.float64, device="cuda", generator=g)
+    V = torch.eye(n, dtype=torch.float64, device="cuda")
+    # warm-up on a copy
+    Gw, Vw = G.clone(), V.clone()
+    eng.sweep(Gw, Vw, 0, min(4, eng.nsteps))
+    torch.cuda.synchronize()
+    for s in range(sweeps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        c = eng.sweep(G, V, 0, steps)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        ns = steps or eng.nsteps
+        rot, proper, key = c.cpu().tolist()
+        print(f"n={n} w={w} sweep {s}: {ms:.1f} ms for {ns} p-steps "
+              f"({ms / ns:.3f} ms/p-step) rot={rot} proper={proper} key={key}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
