@@ -1,0 +1,398 @@
+"""Benchmark: FP64 SVD seconds to convergence (BASELINE.json config 3).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One *step* is one complete solve to convergence -- input factor resident in
+HBM -> sigma, U, V -- of the BASELINE.json config 3 workload: a 16384 x 16384
+FP64 factor, full-block variant, rrow (Mantharam-Eberlein-equivalent)
+strategy, block width 32 (block-columns of 16), V accumulated.  The factor is
+synthetic: G = Q diag(sqrt(lambda)) W^T with a reference type-2 spectrum
+lambda (testgen.gen_spectrum, seed 3) and Haar Q, W generated on the GPU.
+The 2 GiB factor is larger than L2, so no flush is needed between steps.
+
+Prints ONE JSON line (rank 0).  Besides the contract keys it carries
+ - e2e: the same metric through the public API with host (pinned) buffers,
+   host<->device copies inside the timed region;
+ - roofline: the dominant kernel's algorithmic HBM bytes / CUDA-event time;
+ - cpu_baseline: the C oracle (a port of the reference CPU solver) timed on
+   a bounded prefix of the same solve on this host, extrapolated;
+ - accuracy: sigma vs the prescribed spectrum, orthogonality of U and V, and
+   a bitwise check of the GPU against the oracle on that prefix.
+``--impl reference`` times only the CPU oracle on the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "FP64 SVD sec to convergence (n=16384) at 1/2/4/8 B200; σ rel err; sweeps"
+PAPER_K20C_16384_S = 2625.642659  # Table 6.2 (Kepler K20c)
+DEFAULT_SWEEPS_GUESS = 9          # BASELINE.md Table 6.3: 7-12 full-block sweeps
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--n", type=int, default=16384)
+    ap.add_argument("--width", type=int, default=32)
+    ap.add_argument("--variant", default="full-block")
+    ap.add_argument("--strategy", default="rrow")
+    ap.add_argument("--spectrum-type", type=int, default=2)
+    ap.add_argument("--seed", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0,
+                    help="target CPU-oracle sample length")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload(args) -> dict:
+    return {
+        "workload": (f"config3: {args.n}x{args.n} FP64 SVD, {args.variant}, "
+                     f"{args.strategy} strategy (ME-equivalent), block width {args.width} "
+                     f"(block-columns of {args.width // 2}), V accumulated"),
+        "n": args.n, "block_width": args.width, "variant": args.variant,
+        "outer_strategy": args.strategy, "inner_strategy": args.strategy,
+        "input": (f"G = Q diag(sqrt(lambda)) W^T, lambda = type-{args.spectrum_type} spectrum "
+                  f"(seed {args.seed}), Haar Q, W (GPU QR)"),
+        "l2": "inputs larger than L2 (factor 2 GiB per step)",
+    }
+
+
+# ---------------------------------------------------------------------------
+# clocks
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,utilization.gpu,power.draw,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.proc = None
+        self.file = None
+
+    def start(self):
+        try:
+            self.file = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.file, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.file.flush()
+        rows = []
+        for line in Path(self.file.name).read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), float(parts[2]), parts[4:8]))
+            except ValueError:
+                continue
+        os.unlink(self.file.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
+        loaded = [r for r in rows if r[2] >= 50.0] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in loaded for i, v in enumerate(r[3])
+                          if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in loaded),
+                "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons,
+                "samples": len(rows), "samples_under_load": len(loaded)}
+
+
+# ---------------------------------------------------------------------------
+# input
+
+
+def make_input(args):
+    import torch
+
+    from paper_1401_2720_b200.testgen import SpectrumSpec, canonical_sort, gen_factor_device, \
+        gen_spectrum
+
+    lam = gen_spectrum(SpectrumSpec(args.spectrum_type, args.n, args.seed))
+    lam_sorted, n_plus = canonical_sort(lam)
+    sigma = np.sqrt(np.abs(lam_sorted))
+    G0 = gen_factor_device(sigma, seed=args.seed)
+    torch.cuda.synchronize()
+    return G0, sigma, n_plus
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (oracle = C port of the reference solver)
+
+
+def cpu_sample(G0_host_t, args, target_s: float, check_against=None):
+    """Time p-steps of sweep 1 with the C oracle on all host cores.  Returns
+    (seconds per p-step, timed p-steps, cores, oracle state after the
+    sample) -- the state lets the caller compare the GPU bitwise."""
+    from oracle import oracle as O
+    from paper_1401_2720_b200.strategy import as_table, make_strategy
+
+    n = args.n
+    w = args.width
+    cfg = dict(block_width=w, variant=args.variant)
+    outer = as_table(make_strategy(args.strategy, n // (w // 2)))
+    inner = as_table(make_strategy(args.strategy, w))
+    g = np.array(G0_host_t, copy=True).T  # F-order m x n
+    v = np.asfortranarray(np.eye(n))
+    threads = O.max_threads()
+    t0 = time.perf_counter()
+    O.block_sweep(g, v, n, cfg, outer[:1], inner, threads=threads)  # warm, p-step 0
+    t1 = time.perf_counter() - t0
+    k = int(max(1, min(outer.shape[0] - 1, math.ceil(target_s / max(t1, 1e-3)))))
+    t0 = time.perf_counter()
+    O.block_sweep(g, v, n, cfg, outer[1:1 + k], inner, threads=threads)
+    tk = time.perf_counter() - t0
+    return tk / k, k, threads, g, v
+
+
+def read_sweeps_hint() -> int:
+    for p in sorted((ROOT / "profiles").glob("*/bench*.json"), reverse=True):
+        try:
+            d = json.loads(p.read_text())
+            if d.get("impl", "ours") == "ours" and d.get("sweeps"):
+                return int(d["sweeps"])
+        except Exception:
+            continue
+    return DEFAULT_SWEEPS_GUESS
+
+
+# ---------------------------------------------------------------------------
+
+
+def run_reference(args, rank: int):
+    if rank != 0:
+        return
+    import torch
+
+    from oracle import oracle as O
+
+    cfgd = workload(args)
+    if torch.cuda.is_available():
+        G0, _, _ = make_input(args)  # input synthesis only (not the measured path)
+        host = G0.cpu().numpy()
+        del G0
+    else:
+        raise SystemExit("input synthesis needs the GPU")
+    sweeps = read_sweeps_hint()
+    b = args.n // (args.width // 2)
+    per = []
+    for i in range(args.warmup + args.steps):
+        t_p, k, threads, _, _ = cpu_sample(host, args, args.cpu_seconds if i >= args.warmup
+                                           else 1.0)
+        if i >= args.warmup:
+            per.append(t_p)
+    t_p = statistics.mean(per)
+    value = t_p * (b - 1) * sweeps
+    line = {
+        "metric": METRIC, "value": value, "unit": "s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "config": cfgd, "impl": "reference",
+        "cpu_baseline": {
+            "value": value, "unit": "s", "cores": threads, "kind": "port",
+            "sample": (f"C oracle (port of the reference numba solver) on {k} p-steps of "
+                       f"sweep 1 (of {b - 1}), {t_p:.3f} s/p-step, extrapolated x{b - 1} "
+                       f"p-steps x {sweeps} sweeps")},
+        "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    _ = O
+
+
+def run_ours(args, rank: int, world: int):
+    import torch
+
+    from paper_1401_2720_b200 import _lib
+    from paper_1401_2720_b200.driver import Solver, SolverConfig
+    import paper_1401_2720_b200 as J
+
+    if world > 1:
+        raise SystemExit("multi-GPU bench: use the distributed path (not in this build)")
+    lib = _lib.require_cuda()
+    cfg = SolverConfig(block_width=args.width, variant=args.variant,
+                       outer_strategy=args.strategy, inner_strategy=args.strategy)
+    G0, sigma_true, n_plus = make_input(args)
+    n = m = args.n
+    solver = Solver(n, cfg, J.Signature(n, n_plus))
+    eng = solver.engine
+
+    # warm-up steps (full solves)
+    for _ in range(args.warmup):
+        out = solver.solve_device(G0)
+        del out
+    torch.cuda.synchronize()
+
+    # timed steps
+    sampler = ClockSampler(torch.cuda.current_device())
+    sampler.start()
+    launches0 = lib.jh_launch_count()
+    nlaunch_cap = 4 * (eng.nsteps + 8) * cfg.max_block_sweeps * args.steps
+    lib.jh_profile_begin(nlaunch_cap)
+    times = []
+    rotated_tasks = 0
+    gram_launches = 0
+    res = None
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        res = solver.solve_device(G0)
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) / 1e3)
+        rotated_tasks += sum(eng.tasks_rotated)
+        gram_launches += len(res[3]) * eng.nsteps
+    import ctypes
+
+    ms = (ctypes.c_double * 3)()
+    cnt = (ctypes.c_int64 * 3)()
+    lib.jh_profile_end(ms, cnt)
+    launches = lib.jh_launch_count() - launches0
+    clocks = sampler.stop()
+    sigma, U, V, stats, converged = res
+    value = statistics.mean(times)
+
+    # roofline of the dominant streaming kernel
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    w = args.width
+    ntask = n // w
+    bytes_gram_launch = ntask * 8.0 * w * m
+    bytes_update_total = rotated_tasks * 16.0 * w * (m + n)
+    classes = {
+        "gram": {"ms": ms[0], "launches": cnt[0],
+                 "bytes_total": bytes_gram_launch * cnt[0],
+                 "flops_total": ntask * m * w * (w + 1.0) * cnt[0]},
+        "factor_inner": {"ms": ms[1], "launches": cnt[1], "bytes_total": 0.0},
+        "update": {"ms": ms[2], "launches": cnt[2], "bytes_total": bytes_update_total,
+                   "flops_total": rotated_tasks * 2.0 * w * w * (m + n)},
+    }
+    tot_ms = sum(c["ms"] for c in classes.values()) or 1.0
+    dom = max(("gram", "update"), key=lambda k: classes[k]["ms"])
+    d = classes[dom]
+    achieved = d["bytes_total"] / (d["ms"] / 1e3) / 1e9 if d["ms"] > 0 else 0.0
+    traffic = None
+    tp = ROOT / "profiles" / "ncu_traffic.json"
+    if tp.exists():
+        traffic = json.loads(tp.read_text()).get(dom)
+    roofline = {
+        "kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+        "frac": achieved / hbm_peak, "traffic": traffic,
+        "bytes_per_launch": d["bytes_total"] / max(d["launches"], 1),
+        "avg_launch_ms": d["ms"] / max(d["launches"], 1),
+        "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
+        "kernel_share": {k: c["ms"] / tot_ms for k, c in classes.items()},
+        "solve_bytes": classes["gram"]["bytes_total"] + bytes_update_total,
+        "solve_hbm_frac": ((classes["gram"]["bytes_total"] + bytes_update_total)
+                           / (sum(times)) / 1e9 / hbm_peak),
+    }
+
+    # accuracy (outside the timed region)
+    sig = sigma.cpu().numpy()
+    rel = float(np.max(np.abs(sig - sigma_true) / sigma_true))
+    eye = torch.eye(n, dtype=torch.float64, device=U.device)
+    ortho_u = float((U @ U.t() - eye).abs().max())
+    ortho_v = float((V @ V.t() - eye).abs().max())
+    del eye
+    accuracy = {"sigma_max_rel_err_vs_prescribed": rel,
+                "u_orth_max": ortho_u, "v_orth_max": ortho_v,
+                "n_eps": n * 2.0 ** -53}
+    del U, V, res
+
+    # CPU baseline (bounded oracle sample) + bitwise prefix parity
+    cpu = None
+    parity = None
+    if not args.no_cpu:
+        host = G0.cpu().numpy()
+        t_p, k, threads, g_or, v_or = cpu_sample(host, args, args.cpu_seconds)
+        b = n // (w // 2)
+        cpu = {"value": t_p * (b - 1) * len(stats), "unit": "s", "cores": threads,
+               "kind": "port",
+               "sample": (f"C oracle (port of the reference numba solver): p-steps 1..{k} of "
+                          f"sweep 1 ({t_p:.3f} s/p-step), extrapolated x{b - 1} p-steps x "
+                          f"{len(stats)} sweeps")}
+        Gp = G0.clone()
+        Vp = torch.eye(n, dtype=torch.float64, device=G0.device)
+        eng.sweep(Gp, Vp, 0, 1 + k)
+        torch.cuda.synchronize()
+        same_g = bool(np.array_equal(Gp.cpu().numpy(), np.ascontiguousarray(g_or.T)))
+        same_v = bool(np.array_equal(Vp.cpu().numpy(), np.ascontiguousarray(v_or.T)))
+        parity = {"psteps": 1 + k, "G_bitwise_equal": same_g, "V_bitwise_equal": same_v}
+        del Gp, Vp, host, g_or, v_or
+
+    # end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        host_in = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
+        host_in.copy_(G0)
+        g_host = host_in.t()  # m x n, column-major, pinned
+        del G0
+        torch.cuda.empty_cache()
+        et = []
+        for _ in range(args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = J.block_jacobi(g_host, J.Signature(n, n_plus), cfg)
+            et.append(time.perf_counter() - t0)
+            del r
+        e2e = {"value": statistics.mean(et), "unit": "s", "h2d_bytes_per_step": 8 * m * n,
+               "d2h_bytes_per_step": 8 * (n + m * n + n * n)}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,
+        "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": value / PAPER_K20C_16384_S,
+        "dtype": "f64", "data": "synthetic", "config": workload(args),
+        "sweeps": len(stats), "converged": converged, "stats": stats,
+        "accuracy": accuracy, "parity_prefix": parity,
+        "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
+        "clocks": clocks, "gpu_launches": int(launches),
+        "per_step_s": times,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    run_ours(args, rank, world)
+
+
+if __name__ == "__main__":
+    main()

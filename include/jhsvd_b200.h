@@ -43,8 +43,9 @@ int64_t jh_sweep_workspace_bytes(int64_t n, int w);
  * post-multiplication of [Gp Gq] and [Vp Vq] (:407-428).
  *   G  m x n (ld ldg), V nv x n (ld ldv) or NULL; updated in place.
  *   w  block width (shortened order), even, 2 <= w <= 64, n % w == 0.
- *   counters: uint64[3] device: [0] += rotations, [1] += proper rotations,
- *     [2] = min error key (initialise to UINT64_MAX); key layout
+ *   counters: uint64[4] device: [0] += rotations, [1] += proper rotations,
+ *     [2] = min error key (initialise to UINT64_MAX), [3] += tasks that
+ *     rotated (their pair columns were post-multiplied); key layout
  *     p-step<<38 | task<<16 | status<<13 | 1-based index, status 1 =
  *     Cholesky pivot, 2 = zero column, 3 = hyperbolic domain.
  */
@@ -94,6 +95,13 @@ int jh_check_scaling(const double *G, int64_t ldg, int64_t m, int64_t n,
  * init UINT64_MAX) = smallest 1-based zero column. */
 int jh_sigma_u(const double *G, int64_t ldg, int64_t m, int64_t n, double *sigma, double *U,
                int64_t ldu, unsigned long long *bad, void *stream);
+
+/* Launch accounting / per-kernel-class timing (bench.py): classes are
+ * 0 Gram, 1 factor + inner Jacobi, 2 update.  jh_profile_end synchronizes
+ * on the recorded events. */
+unsigned long long jh_launch_count(void);
+int jh_profile_begin(int max_launches);
+int jh_profile_end(double *ms, int64_t *count);
 
 /* Diagnostic: DMMA (mma.sync m8n8k4 f64) vs in-order fma chain. */
 int jh_probe_dmma(const double *A, const double *B, const double *C, double *Dm, double *Df,

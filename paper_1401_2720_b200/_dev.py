@@ -23,6 +23,14 @@ def is_torch(a) -> bool:
     return isinstance(a, torch.Tensor)
 
 
+def out_mode(a) -> str:
+    """How results are returned for input `a`: 'numpy', 'device' (CUDA
+    tensors) or 'host' (CPU torch tensors, pinned when large)."""
+    if not is_torch(a):
+        return "numpy"
+    return "device" if a.is_cuda else "host"
+
+
 def to_colmajor(a, copy: bool = False) -> torch.Tensor:
     """m x n host or device matrix -> (n, m) contiguous FP64 device tensor."""
     if is_torch(a):
@@ -42,12 +50,29 @@ def to_colmajor(a, copy: bool = False) -> torch.Tensor:
     return host.to(device(), non_blocking=True)
 
 
-def from_colmajor(t: torch.Tensor, as_numpy: bool):
-    """(n, m) column-major storage -> m x n result (numpy F-order or torch view)."""
-    if not as_numpy:
-        return t.t()
-    return np.asfortranarray(t.cpu().numpy().T)
+def _to_host(t: torch.Tensor) -> torch.Tensor:
+    if t.numel() >= (1 << 20):
+        out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        out.copy_(t, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return out
+    return t.cpu()
 
 
-def vector_out(t: torch.Tensor, as_numpy: bool):
-    return t.cpu().numpy() if as_numpy else t
+def from_colmajor(t: torch.Tensor, mode):
+    """(n, m) column-major storage -> m x n result: numpy F-order array
+    ('numpy' / True), CUDA tensor view ('device' / False) or CPU tensor
+    view ('host')."""
+    if mode is True or mode == "numpy":
+        return np.asfortranarray(_to_host(t).numpy().T)
+    if mode == "host":
+        return _to_host(t).t()
+    return t.t()
+
+
+def vector_out(t: torch.Tensor, mode):
+    if mode is True or mode == "numpy":
+        return t.cpu().numpy()
+    if mode == "host":
+        return t.cpu()
+    return t

@@ -140,7 +140,7 @@ def inner_jacobi(r, colmap, signature: Signature, strategy: PStrategy, max_sweep
         raise ValueError("inner_jacobi on the GPU supports orders up to 64")
     signs = torch.tensor([signature.sign(int(g)) for g in colmap], dtype=torch.int8,
                          device=rt.device)
-    steps = torch.from_numpy(np.ascontiguousarray(as_table(strategy))).to(rt.device)
+    steps = torch.from_numpy(np.array(as_table(strategy))).to(rt.device)
     v = torch.empty_like(rt)
     out = torch.zeros(5, dtype=torch.int64, device=rt.device)
     tol_c = EPS * math.sqrt(c) * eps_factor

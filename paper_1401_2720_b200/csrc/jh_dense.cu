@@ -118,6 +118,7 @@ extern "C" {
 // gram (blockkernel.py:99-107): H (c x c) = A^T A, A m x c (ld lda).
 int jh_gram(const double *A, int64_t lda, int64_t m, int c, double *H, void *stream) {
   const int nt = (int)cdiv(c, kSyrkT);
+  g_launches++;
   k_syrk_exact<<<nt * (nt + 1) / 2, 256, 0, (cudaStream_t)stream>>>(A, lda, m, c, H);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : -(int)e;
@@ -127,6 +128,7 @@ int jh_gram(const double *A, int64_t lda, int64_t m, int c, double *H, void *str
 int jh_gemm(const double *A, int64_t lda, int64_t m, int k, const double *B, int64_t ldb, int n2,
             double *C, int64_t ldc, void *stream) {
   dim3 grid((unsigned)cdiv(m, 64), (unsigned)cdiv(n2, 32));
+  g_launches++;
   k_gemm_exact<<<grid, 256, 0, (cudaStream_t)stream>>>(A, lda, m, k, B, ldb, n2, C, ldc);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : -(int)e;
@@ -135,6 +137,7 @@ int jh_gemm(const double *A, int64_t lda, int64_t m, int k, const double *B, int
 // solve_for_v back substitution (driver.py:203-211), R n x n upper, W n x nc.
 int jh_back_substitute(const double *R, int n, const double *W, int nc, double *out,
                        void *stream) {
+  g_launches++;
   k_back_substitute<<<(unsigned)cdiv(nc, 128), 128, 0, (cudaStream_t)stream>>>(R, n, W, nc, out);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : -(int)e;

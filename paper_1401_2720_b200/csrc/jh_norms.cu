@@ -342,6 +342,7 @@ int jh_column_norms(const double *G, int64_t ldg, int64_t m, int64_t n, int64_t 
   double mu, nu;
   jh_safe_bounds(m, &mu, &nu);
   prep_norm(m);
+  g_launches++;
   k_colnorm<<<(unsigned)n, kNormThreads, norm_smem(m), (cudaStream_t)stream>>>(
       G, ldg, m, n, mu, nu, 0, 0.0, 0.0, js, s, nullptr, 0, nullptr);
   const cudaError_t e = cudaGetLastError();
@@ -356,6 +357,7 @@ int jh_check_scaling(const double *G, int64_t ldg, int64_t m, int64_t n,
   double mu, nu;
   jh_safe_bounds(m, &mu, &nu);
   prep_norm(m);
+  g_launches++;
   k_colnorm<<<(unsigned)n, kNormThreads, norm_smem(m), (cudaStream_t)stream>>>(
       G, ldg, m, n, mu, nu, 1, mu, std::sqrt(nu), nullptr, nullptr, nullptr, 0, bad);
   const cudaError_t e = cudaGetLastError();
@@ -369,6 +371,7 @@ int jh_sigma_u(const double *G, int64_t ldg, int64_t m, int64_t n, double *sigma
   double mu, nu;
   jh_safe_bounds(m, &mu, &nu);
   prep_norm(m);
+  g_launches++;
   k_colnorm<<<(unsigned)n, kNormThreads, norm_smem(m), (cudaStream_t)stream>>>(
       G, ldg, m, n, mu, nu, 2, 0.0, 0.0, nullptr, sigma, U, ldu, bad);
   const cudaError_t e = cudaGetLastError();

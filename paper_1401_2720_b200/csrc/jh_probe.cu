@@ -39,6 +39,7 @@ extern "C" int jh_probe_dmma(const double *A, const double *B, const double *C, 
                              double *Df, int ntests, void *stream) {
   const int threads = 256;
   const int blocks = (ntests * 32 + threads - 1) / threads;
+  jh::g_launches++;
   jh::k_probe_dmma<<<blocks, threads, 0, (cudaStream_t)stream>>>(A, B, C, Dm, Df, ntests);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : -(int)e;

@@ -273,7 +273,7 @@ __device__ InnerOut cta_inner_jacobi(double *R, double *V, int w, const int32_t 
 // K2: Cholesky + inner Jacobi for every task of the p-step; one CTA of
 // 32 * max(1, w/2) threads per task.  Dynamic smem: H/R and V (2 w^2 doubles).
 //   counters[0] += rotations, counters[1] += proper rotations,
-//   counters[2] = min error key (ULLONG_MAX when clean)
+//   counters[2] = min error key (ULLONG_MAX when clean), counters[3] += tasks rotated
 __global__ void k_factor_inner(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
                                int64_t *__restrict__ task_rot, const int32_t *__restrict__ pairs,
                                int bw, int64_t n_plus, const int32_t *__restrict__ inner,
@@ -330,6 +330,7 @@ __global__ void k_factor_inner(const double *__restrict__ Hbuf, double *__restri
     task_rot[task] = o.rot;
     atomicAdd(&counters[0], (unsigned long long)o.rot);
     atomicAdd(&counters[1], (unsigned long long)o.proper);
+    if (o.rot) atomicAdd(&counters[3], 1ull);
   }
 }
 
@@ -427,11 +428,74 @@ __global__ void k_inner_single(double *__restrict__ R, double *__restrict__ V, i
   }
 }
 
+// ---------------------------------------------------------------------------
+// Launch accounting and optional per-kernel-class event timing (bench.py).
+
+struct Profiler {
+  bool on = false;
+  int cap = 0, used = 0;
+  cudaEvent_t *ev = nullptr;  // pairs (before, after)
+  int *cls = nullptr;
+};
+static Profiler g_prof;
+unsigned long long g_launches = 0;
+
+static inline void prof_mark(cudaStream_t st, int cls, bool after) {
+  if (!g_prof.on) return;
+  if (!after) {
+    if (g_prof.used >= g_prof.cap) return;
+    cudaEventRecord(g_prof.ev[2 * g_prof.used], st);
+    g_prof.cls[g_prof.used] = cls;
+  } else {
+    if (g_prof.used >= g_prof.cap) return;
+    cudaEventRecord(g_prof.ev[2 * g_prof.used + 1], st);
+    g_prof.used++;
+  }
+}
+
 }  // namespace jh
 
 using namespace jh;
 
 extern "C" {
+
+// Number of kernels this library has launched (all entry points).
+unsigned long long jh_launch_count(void) { return g_launches; }
+
+// Start timing every p-step kernel launch (up to max_launches launches).
+int jh_profile_begin(int max_launches) {
+  if (g_prof.cap < max_launches) {
+    for (int i = 0; i < 2 * g_prof.cap; i++) cudaEventDestroy(g_prof.ev[i]);
+    delete[] g_prof.ev;
+    delete[] g_prof.cls;
+    g_prof.ev = new cudaEvent_t[2 * (size_t)max_launches];
+    g_prof.cls = new int[max_launches];
+    for (int i = 0; i < 2 * max_launches; i++) cudaEventCreate(&g_prof.ev[i]);
+    g_prof.cap = max_launches;
+  }
+  g_prof.used = 0;
+  g_prof.on = true;
+  return 0;
+}
+
+// Stop timing; synchronizes on the recorded events and returns per kernel
+// class (0 gram, 1 factor+inner, 2 update) the summed milliseconds and the
+// number of timed launches.
+int jh_profile_end(double *ms, int64_t *count) {
+  g_prof.on = false;
+  for (int k = 0; k < 3; k++) {
+    ms[k] = 0.0;
+    count[k] = 0;
+  }
+  for (int i = 0; i < g_prof.used; i++) {
+    float t = 0.f;
+    cudaEventSynchronize(g_prof.ev[2 * i + 1]);
+    cudaEventElapsedTime(&t, g_prof.ev[2 * i], g_prof.ev[2 * i + 1]);
+    ms[g_prof.cls[i]] += t;
+    count[g_prof.cls[i]]++;
+  }
+  return 0;
+}
 
 // Bytes of device workspace jh_block_sweep needs for order n and width w.
 int64_t jh_sweep_workspace_bytes(int64_t n, int w) {
@@ -476,12 +540,19 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
   }
   for (int s = first_step; s < first_step + nsteps; s++) {
     const int32_t *pairs = outer + (int64_t)s * ntask * 2;
+    prof_mark(st, 0, false);
     k_gram<<<ntask, kGramThreads, smem_gram, st>>>(G, ldg, m, pairs, bw, Hbuf);
+    prof_mark(st, 0, true);
+    prof_mark(st, 1, false);
     k_factor_inner<<<ntask, thr_inner, smem_inner, st>>>(Hbuf, Vbuf, trot, pairs, bw, n_plus, inner,
                                                  inner_limit, tol_c, counters, s);
+    prof_mark(st, 1, true);
     dim3 grid(ntask, nbg + nbv);
+    prof_mark(st, 2, false);
     k_update<<<grid, kUpdThreads, smem_upd, st>>>(G, ldg, m, V, ldv, nv, pairs, bw, Vbuf, trot,
                                                   nbg);
+    prof_mark(st, 2, true);
+    g_launches += 3;
   }
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : -(int)e;
@@ -491,6 +562,7 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
 // overwritten) and writes R = L^T (zero strict lower) to R; *info (device)
 // = 0 or the 1-based bad pivot.
 int jh_cholesky(double *H, int c, double *R, int *info, void *stream) {
+  g_launches++;
   k_cholesky_single<<<1, 1024, 0, (cudaStream_t)stream>>>(H, c, R, info);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : -(int)e;
@@ -507,6 +579,7 @@ int jh_inner_jacobi(double *R, double *V, int c, const int32_t *steps, const int
                          (int)(sizeof(double) * 2 * kMaxW * kMaxW));
     attr = true;
   }
+  g_launches++;
   k_inner_single<<<1, 32 * (c / 2), smem, (cudaStream_t)stream>>>(R, V, c, steps, signs, tol_c,
                                                                   max_sweeps, out);
   const cudaError_t e = cudaGetLastError();

@@ -118,19 +118,19 @@ class SweepEngine:
         self.cfg = cfg
         self.outer = outer
         self.n_plus = int(n_plus)
-        self.outer_dev = torch.from_numpy(np.ascontiguousarray(as_table(outer))).to(dev)
-        self.inner_dev = torch.from_numpy(np.ascontiguousarray(as_table(inner))).to(dev)
+        self.outer_dev = torch.from_numpy(np.array(as_table(outer))).to(dev)
+        self.inner_dev = torch.from_numpy(np.array(as_table(inner))).to(dev)
         self.nsteps = outer.num_steps
         nbytes = int(self.lib.jh_sweep_workspace_bytes(n, w))
         self.ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
-        self.counters = torch.empty(3, dtype=torch.int64, device=dev)
+        self.counters = torch.empty(4, dtype=torch.int64, device=dev)
         self.tol_c = EPS * math.sqrt(w) * cfg.eps_factor
 
     def sweep(self, G, V, first_step: int = 0, nsteps: Optional[int] = None):
         """Enqueue p-steps [first_step, first_step + nsteps) of one block
         sweep on G (n, m) / V (n, nv) column-major tensors; returns the
         device counter tensor (rotations, proper, error key)."""
-        self.counters[0:2].zero_()
+        self.counters.zero_()
         self.counters[2].fill_(-1)
         ns = self.nsteps - first_step if nsteps is None else nsteps
         rc = self.lib.jh_block_sweep(
@@ -164,11 +164,13 @@ class SweepEngine:
         """Sweep loop of run_block_jacobi_inplace (driver.py:176-200)."""
         stats: list[tuple[int, int]] = []
         converged = False
+        self.tasks_rotated: list[int] = []
         for _ in range(self.cfg.max_block_sweeps):
-            rot, proper, key = (int(x) for x in self.sweep(G, V).cpu().tolist())
+            rot, proper, key, nrot = (int(x) for x in self.sweep(G, V).cpu().tolist())
             if key != -1:
                 self.raise_error(key)
             stats.append((rot, proper))
+            self.tasks_rotated.append(nrot)
             if proper == 0:
                 converged = True
                 break
@@ -386,10 +388,10 @@ def block_jacobi(g, signature: Optional[Signature] = None, cfg: SolverConfig = S
     inside each signature class (+ class first) with U and V permuted
     consistently; g = U diag(sigma) V^T for J = I.
 
-    Host (numpy) input -> numpy outputs; CUDA tensor input -> CUDA tensor
-    outputs.  ``allow_tall`` (an extension; the reference is square-only)
+    Host numpy input -> numpy outputs; CUDA tensor input -> CUDA tensor
+    outputs; CPU tensor input (pinned for speed) -> CPU tensor outputs.  ``allow_tall`` (an extension; the reference is square-only)
     accepts m > n factors."""
-    as_np = not _dev.is_torch(g)
+    mode = _dev.out_mode(g)
     shape = tuple(int(s) for s in g.shape)
     if len(shape) != 2 or (shape[1] != shape[0] and not (allow_tall and shape[0] > shape[1])):
         raise ValueError("the input factor must be square")
@@ -405,9 +407,9 @@ def block_jacobi(g, signature: Optional[Signature] = None, cfg: SolverConfig = S
     solver = Solver(n, cfg, signature, m=m)
     sigma, U, V, stats, converged = solver.solve_device(G0)
     return HsvdResult(
-        sigma=_dev.vector_out(sigma, as_np),
-        u=_dev.from_colmajor(U, as_np),
-        v=_dev.from_colmajor(V, as_np) if V is not None else None,
+        sigma=_dev.vector_out(sigma, mode),
+        u=_dev.from_colmajor(U, mode),
+        v=_dev.from_colmajor(V, mode) if V is not None else None,
         signature=signature,
         stats=tuple(stats),
         block_sweeps=len(stats),
