@@ -1,0 +1,20 @@
+// Host-side launchers shared between the translation units of the library.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace jh {
+
+// DMMA/TMA Gram of every task of a p-step (jh_tiles.cu); w in {16, 32}.
+bool gram_tma_ok(int w, int64_t m, int64_t ldg);
+void launch_gram_tma(const double *G, int64_t ldg, int64_t m, const int32_t *pairs, int ntask,
+                     int w, double *Hbuf, cudaStream_t st);
+
+// DMMA post-multiplication of every rotated task's pair columns (jh_tiles.cu).
+bool update_dmma_ok(int w);
+void launch_update_dmma(double *G, int64_t ldg, int64_t m, double *V, int64_t ldv, int64_t nv,
+                        const int32_t *pairs, int ntask, int w, const double *Vbuf,
+                        const int64_t *trot, cudaStream_t st);
+
+}  // namespace jh

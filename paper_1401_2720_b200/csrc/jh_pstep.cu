@@ -16,8 +16,10 @@
 // starting at p*bw.  Per-task scratch (H, V', rotation counts) is a small
 // workspace that stays L2-resident.
 #include "jh_common.cuh"
+#include "jh_kernels.h"
 
 #include <cstdio>
+#include <cstdlib>
 
 namespace jh {
 
@@ -538,10 +540,17 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
                          (int)(sizeof(double) * 2 * kMaxW * kMaxW));
     attr_set = true;
   }
+  // fast paths (DMMA tiles) unless JHSVD_FORCE_SIMPLE is set (parity tests)
+  static const bool force_simple = getenv("JHSVD_FORCE_SIMPLE") != nullptr;
+  const bool use_tma_gram = !force_simple && gram_tma_ok(w, m, ldg);
+  const bool use_dmma_update = !force_simple && update_dmma_ok(w);
   for (int s = first_step; s < first_step + nsteps; s++) {
     const int32_t *pairs = outer + (int64_t)s * ntask * 2;
     prof_mark(st, 0, false);
-    k_gram<<<ntask, kGramThreads, smem_gram, st>>>(G, ldg, m, pairs, bw, Hbuf);
+    if (use_tma_gram)
+      launch_gram_tma(G, ldg, m, pairs, ntask, w, Hbuf, st);
+    else
+      k_gram<<<ntask, kGramThreads, smem_gram, st>>>(G, ldg, m, pairs, bw, Hbuf);
     prof_mark(st, 0, true);
     prof_mark(st, 1, false);
     k_factor_inner<<<ntask, thr_inner, smem_inner, st>>>(Hbuf, Vbuf, trot, pairs, bw, n_plus, inner,
@@ -549,8 +558,11 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
     prof_mark(st, 1, true);
     dim3 grid(ntask, nbg + nbv);
     prof_mark(st, 2, false);
-    k_update<<<grid, kUpdThreads, smem_upd, st>>>(G, ldg, m, V, ldv, nv, pairs, bw, Vbuf, trot,
-                                                  nbg);
+    if (use_dmma_update)
+      launch_update_dmma(G, ldg, m, V, ldv, nv, pairs, ntask, w, Vbuf, trot, st);
+    else
+      k_update<<<grid, kUpdThreads, smem_upd, st>>>(G, ldg, m, V, ldv, nv, pairs, bw, Vbuf, trot,
+                                                    nbg);
     prof_mark(st, 2, true);
     g_launches += 3;
   }

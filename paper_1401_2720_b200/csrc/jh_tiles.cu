@@ -1,0 +1,249 @@
+// DMMA-tiled, bitwise-exact Gram and post-multiply kernels of the p-step
+// (the streaming, HBM-bound part of the hot path).
+//
+//   K1  k_gram_tma<W>     H = [Gp Gq]^T [Gp Gq]       (blockkernel.py:76-107)
+//   K3  k_update_dmma<W>  [Gp Gq] <- [Gp Gq] V'       (blockkernel.py:407-428)
+//                          and [Vp Vq] <- [Vp Vq] V'  (driver.py:165-173)
+//
+// Exactness: every output entry is one chain of DMMA k-steps in ascending k,
+// each DMMA being four in-order fmas (see jh_dmma.cuh), from +0.0 -- the
+// reference's per-entry fma chain.  Rows past the end of a column are fed as
+// zeros: fma(0, x, acc) leaves any accumulator that started at +0.0 unchanged
+// (finite data; such a chain never holds -0.0), so padding is bit-neutral.
+#include "jh_dmma.cuh"
+#include "jh_kernels.h"
+
+namespace jh {
+
+// ---------------------------------------------------------------------------
+// K1: Gram matrix of one block-column pair per CTA (one warp).
+//
+// Row chunks of the pair (64 rows x W columns) stream into a 3-stage shared
+// memory ring through the TMA engine (cp.async.bulk, one 512 B copy per
+// column, completion on an mbarrier).  Columns are stored with a padded
+// stride of 68 doubles so that the DMMA fragment loads (lane = (column
+// 8X + g, row 4kk + t)) are bank-conflict free.  The warp owns all
+// (W/8)(W/8+1)/2 lower 8x8 tiles; per k-step it loads W/8 fragments (one
+// LDS.64 each) and issues one DMMA per tile: fragment X serves as the A
+// operand (A^T rows) and the B operand alike.
+
+constexpr int kRch = 64;          // rows per staged chunk
+constexpr int kLd = kRch + 4;     // padded smem column stride (doubles)
+constexpr int kStages = 3;
+
+template <int W>
+__global__ void __launch_bounds__(32)
+k_gram_tma(const double *__restrict__ G, int64_t ldg, int64_t m,
+           const int32_t *__restrict__ pairs, double *__restrict__ Hbuf) {
+  constexpr int NT = W / 8, BW = W / 2, NTILE = NT * (NT + 1) / 2;
+  extern __shared__ __align__(128) double sm[];  // [kStages][W][kLd]
+  __shared__ __align__(8) uint64_t full[kStages];
+  const int task = blockIdx.x, lane = threadIdx.x, g = lane >> 2, t = lane & 3;
+  const int p = pairs[2 * task], q = pairs[2 * task + 1];
+  const int64_t nchunk = cdiv(m, kRch);
+  if (lane == 0) {
+    for (int s = 0; s < kStages; s++) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  auto issue = [&](int64_t c) {
+    const int s = (int)(c % kStages);
+    const int64_t r0 = c * kRch;
+    const uint32_t bytes = (uint32_t)min64(kRch, m - r0) * 8u;
+    if (lane == 0) mbar_expect_tx(&full[s], bytes * W);
+    __syncwarp();
+    for (int j = lane; j < W; j += 32) {
+      const int64_t col = j < BW ? (int64_t)p * BW + j : (int64_t)q * BW + (j - BW);
+      bulk_g2s(sm + ((size_t)s * W + j) * kLd, G + col * ldg + r0, bytes, &full[s]);
+    }
+  };
+  for (int64_t c = 0; c < kStages && c < nchunk; c++) issue(c);
+
+  double acc[NTILE][2];
+#pragma unroll
+  for (int i = 0; i < NTILE; i++) acc[i][0] = acc[i][1] = 0.0;
+
+  for (int64_t c = 0; c < nchunk; c++) {
+    const int s = (int)(c % kStages);
+    mbar_wait(&full[s], (uint32_t)((c / kStages) & 1));
+    const double *buf = sm + (size_t)s * W * kLd + (size_t)g * kLd + t;
+    const int nr = (int)min64(kRch, m - c * kRch);
+    if (nr == kRch) {
+#pragma unroll 4
+      for (int kk = 0; kk < kRch / 4; kk++) {
+        double f[NT];
+#pragma unroll
+        for (int X = 0; X < NT; X++) f[X] = buf[X * 8 * kLd + 4 * kk];
+        int i = 0;
+#pragma unroll
+        for (int X = 0; X < NT; X++)
+#pragma unroll
+          for (int Y = 0; Y <= X; Y++, i++) dmma(acc[i][0], acc[i][1], f[X], f[Y]);
+      }
+    } else {
+      const int nks = (nr + 3) / 4;
+      for (int kk = 0; kk < nks; kk++) {
+        const bool ok = 4 * kk + t < nr;
+        double f[NT];
+#pragma unroll
+        for (int X = 0; X < NT; X++) f[X] = ok ? buf[X * 8 * kLd + 4 * kk] : 0.0;
+        int i = 0;
+#pragma unroll
+        for (int X = 0; X < NT; X++)
+#pragma unroll
+          for (int Y = 0; Y <= X; Y++, i++) dmma(acc[i][0], acc[i][1], f[X], f[Y]);
+      }
+    }
+    __syncwarp();
+    if (c + kStages < nchunk) issue(c + kStages);
+  }
+  double *H = Hbuf + (size_t)task * W * W;  // column-major: H[y * W + x] = h[x][y]
+  int i = 0;
+#pragma unroll
+  for (int X = 0; X < NT; X++)
+#pragma unroll
+    for (int Y = 0; Y <= X; Y++, i++)
+#pragma unroll
+      for (int j = 0; j < 2; j++) {
+        const int x = 8 * X + g, y = 8 * Y + 2 * t + j;
+        H[y * W + x] = acc[i][j];
+        if (X != Y) H[x * W + y] = acc[i][j];
+      }
+}
+
+// ---------------------------------------------------------------------------
+// K3: in-place post-multiplication of the pair columns of G (rows < m) and V
+// (rows < nv) by the task's V' (W x W).  A CTA of 8 warps owns a slab of
+// 8 * kUpdRpw rows of one matrix for one task; V' sits in shared memory in
+// fragment order (conflict-free LDS.64 of the DMMA B operand).  Each warp
+// streams 8-row blocks: W/4 A fragments (LDG.64, rows r0+g, columns 4kk+t),
+// W/4 x W/8 DMMAs and W/4 STG.64 of the result (rows r0+g, columns 8Y+2t+j:
+// every 32 B sector is written whole).  Loads run two blocks ahead.  Every
+// row is read completely before it is written, by the same warp.
+
+constexpr int kUpdWarps = 8;
+constexpr int kUpdRpw = 256;  // rows per warp
+
+template <int W>
+__global__ void __launch_bounds__(32 * kUpdWarps, 1)
+k_update_dmma(double *__restrict__ G, int64_t ldg, int64_t m, double *__restrict__ V,
+              int64_t ldv, int64_t nv, const int32_t *__restrict__ pairs,
+              const double *__restrict__ Vbuf, const int64_t *__restrict__ trot, int nslab_g) {
+  constexpr int NT = W / 8, NK = W / 4, BW = W / 2;
+  __shared__ double vfrag[NK * NT * 32];
+  const int task = blockIdx.x;
+  if (trot[task] == 0) return;
+  const int p = pairs[2 * task], q = pairs[2 * task + 1];
+  double *A;
+  int64_t ld, rows, slab0;
+  if ((int)blockIdx.y < nslab_g) {
+    A = G; ld = ldg; rows = m; slab0 = (int64_t)blockIdx.y * kUpdWarps * kUpdRpw;
+  } else {
+    A = V; ld = ldv; rows = nv; slab0 = (int64_t)(blockIdx.y - nslab_g) * kUpdWarps * kUpdRpw;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  // V' fragments: B[k][n] = v'[4kk + t][8Y + g]; Vbuf is column-major (v'[k][n] at n*W + k)
+  const double *Vt = Vbuf + (size_t)task * W * W;
+  for (int e = threadIdx.x; e < NK * NT * 32; e += blockDim.x) {
+    const int l = e & 31, f = e >> 5, kk = f / NT, Y = f % NT;
+    vfrag[e] = Vt[(8 * Y + (l >> 2)) * W + 4 * kk + (l & 3)];
+  }
+  __syncthreads();
+  const int64_t r_begin = slab0 + (int64_t)warp * kUpdRpw;
+  if (r_begin >= rows) return;
+  const int64_t r_end = min64(r_begin + kUpdRpw, rows);
+
+  // column c of the pair: block p for c < BW, block q otherwise
+  const double *pin = A + ((int64_t)p * BW + t) * ld;
+  const double *qin = A + ((int64_t)q * BW + t) * ld;
+  double *pout = A + ((int64_t)p * BW + 2 * t) * ld;
+  double *qout = A + ((int64_t)q * BW + 2 * t) * ld;
+  auto ain = [&](int kk) -> const double * {
+    return kk < NK / 2 ? pin + (int64_t)(4 * kk) * ld : qin + (int64_t)(4 * kk - BW) * ld;
+  };
+  auto aout = [&](int Y, int j) -> double * {
+    return Y < NT / 2 ? pout + (int64_t)(8 * Y + j) * ld : qout + (int64_t)(8 * Y + j - BW) * ld;
+  };
+  auto load_block = [&](int64_t r0, double (&f)[NK]) {
+    const int64_t row = r0 + g;
+    const bool ok = row < r_end;
+#pragma unroll
+    for (int kk = 0; kk < NK; kk++) f[kk] = ok ? ld_f64(ain(kk) + row) : 0.0;
+  };
+  auto compute_store = [&](int64_t r0, const double (&f)[NK]) {
+    double acc[NT][2];
+#pragma unroll
+    for (int Y = 0; Y < NT; Y++) acc[Y][0] = acc[Y][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < NK; kk++)
+#pragma unroll
+      for (int Y = 0; Y < NT; Y++)
+        dmma(acc[Y][0], acc[Y][1], f[kk], vfrag[(kk * NT + Y) * 32 + lane]);
+    const int64_t row = r0 + g;
+    if (row < r_end) {
+#pragma unroll
+      for (int Y = 0; Y < NT; Y++)
+#pragma unroll
+        for (int j = 0; j < 2; j++) st_f64(aout(Y, j) + row, acc[Y][j]);
+    }
+  };
+  double f0[NK], f1[NK], f2[NK];
+  load_block(r_begin, f0);
+  load_block(r_begin + 8, f1);
+  for (int64_t r0 = r_begin; r0 < r_end; r0 += 24) {
+    load_block(r0 + 16, f2);
+    compute_store(r0, f0);
+    if (r0 + 8 >= r_end) break;
+    load_block(r0 + 24, f0);
+    compute_store(r0 + 8, f1);
+    if (r0 + 16 >= r_end) break;
+    load_block(r0 + 32, f1);
+    compute_store(r0 + 16, f2);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+
+bool gram_tma_ok(int w, int64_t m, int64_t ldg) {
+  return (w == 16 || w == 32) && m % 2 == 0 && ldg % 2 == 0;
+}
+
+template <int W>
+static void launch_gram_t(const double *G, int64_t ldg, int64_t m, const int32_t *pairs,
+                          int ntask, double *Hbuf, cudaStream_t st) {
+  const size_t smem = sizeof(double) * (size_t)kStages * W * kLd;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_gram_tma<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_gram_tma<W><<<ntask, 32, smem, st>>>(G, ldg, m, pairs, Hbuf);
+}
+
+void launch_gram_tma(const double *G, int64_t ldg, int64_t m, const int32_t *pairs, int ntask,
+                     int w, double *Hbuf, cudaStream_t st) {
+  if (w == 16)
+    launch_gram_t<16>(G, ldg, m, pairs, ntask, Hbuf, st);
+  else
+    launch_gram_t<32>(G, ldg, m, pairs, ntask, Hbuf, st);
+}
+
+bool update_dmma_ok(int w) { return w == 16 || w == 32; }
+
+void launch_update_dmma(double *G, int64_t ldg, int64_t m, double *V, int64_t ldv, int64_t nv,
+                        const int32_t *pairs, int ntask, int w, const double *Vbuf,
+                        const int64_t *trot, cudaStream_t st) {
+  const int64_t slab = (int64_t)kUpdWarps * kUpdRpw;
+  const int nsg = (int)cdiv(m, slab);
+  const int nsv = V ? (int)cdiv(nv, slab) : 0;
+  dim3 grid(ntask, nsg + nsv);
+  if (w == 16)
+    k_update_dmma<16><<<grid, 32 * kUpdWarps, 0, st>>>(G, ldg, m, V, ldv, nv, pairs, Vbuf, trot,
+                                                        nsg);
+  else
+    k_update_dmma<32><<<grid, 32 * kUpdWarps, 0, st>>>(G, ldg, m, V, ldv, nv, pairs, Vbuf, trot,
+                                                        nsg);
+}
+
+}  // namespace jh

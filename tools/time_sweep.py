@@ -30,7 +30,13 @@ def main():
     Gw, Vw = G.clone(), V.clone()
     eng.sweep(Gw, Vw, 0, min(4, eng.nsteps))
     torch.cuda.synchronize()
+    import ctypes
+
+    from paper_1401_2720_b200 import _lib
+
+    lib = _lib.load_library()
     for s in range(sweeps):
+        lib.jh_profile_begin(4 * eng.nsteps + 16)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         c = eng.sweep(G, V, 0, steps)
@@ -38,9 +44,25 @@ def main():
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
         ns = steps or eng.nsteps
-        rot, proper, key = c.cpu().tolist()
+        rot, proper, key, nrot = c.cpu().tolist()
+        pms = (ctypes.c_double * 3)()
+        pcnt = (ctypes.c_int64 * 3)()
+        lib.jh_profile_end(pms, pcnt)
         print(f"n={n} w={w} sweep {s}: {ms:.1f} ms for {ns} p-steps "
-              f"({ms / ns:.3f} ms/p-step) rot={rot} proper={proper} key={key}", flush=True)
+              f"({ms / ns:.3f} ms/p-step) rot={rot} proper={proper} key={key} "
+              f"rotated_tasks={nrot}", flush=True)
+        names = ("gram", "factor_inner", "update")
+        ntask = n // w
+        for k in range(3):
+            per = pms[k] / max(pcnt[k], 1)
+            extra = ""
+            if k == 0:
+                gbs = ntask * 8.0 * w * n / (per / 1e3) / 1e9
+                extra = f" {gbs:.0f} GB/s"
+            if k == 2:
+                gbs = nrot * 16.0 * w * 2 * n / (pms[k] / 1e3) / 1e9
+                extra = f" {gbs:.0f} GB/s"
+            print(f"   {names[k]:13s} {pms[k]:9.2f} ms total, {per * 1e3:9.1f} us/launch{extra}")
 
 
 if __name__ == "__main__":
