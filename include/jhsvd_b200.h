@@ -107,6 +107,10 @@ int jh_profile_end(double *ms, int64_t *count);
 int jh_probe_dmma(const double *A, const double *B, const double *C, double *Dm, double *Df,
                   int ntests, void *stream);
 
+/* Diagnostic: sustained DMMA (kind 0) / DFMA (kind 1) issue rate; each warp
+ * runs 8 independent chains for `iters` iterations. */
+int jh_probe_rate(int kind, int ctas, int threads, int iters, double *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

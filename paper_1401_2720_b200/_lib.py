@@ -39,6 +39,7 @@ SIGNATURES = {
     "jh_check_scaling": (_c_i32, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p]),
     "jh_sigma_u": (_c_i32, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_i64, _c_p, _c_p]),
     "jh_probe_dmma": (_c_i32, [_c_p, _c_p, _c_p, _c_p, _c_p, _c_i32, _c_p]),
+    "jh_probe_rate": (_c_i32, [_c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_p]),
     "jh_launch_count": (ctypes.c_ulonglong, []),
     "jh_profile_begin": (_c_i32, [_c_i32]),
     "jh_profile_end": (_c_i32, [_c_p, _c_p]),

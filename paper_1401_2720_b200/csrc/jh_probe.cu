@@ -44,3 +44,53 @@ extern "C" int jh_probe_dmma(const double *A, const double *B, const double *C, 
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : -(int)e;
 }
+
+// Diagnostic: sustained DMMA / DFMA issue rate.  Each warp runs 8 independent
+// accumulator chains for `iters` iterations (8 DMMA or 8x? DFMA per
+// iteration); the host times the launch to get FMA/s.
+namespace jh {
+__global__ void k_rate_dmma(int iters, double *out) {
+  const int lane = threadIdx.x & 31;
+  double a = 1.0 + lane * 1e-3, b = 1.0 - lane * 1e-3;
+  double d[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; i++) d[i][0] = d[i][1] = 0.0;
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int i = 0; i < 8; i++)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(d[i][0]), "+d"(d[i][1])
+                   : "d"(a), "d"(b));
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; i++) s += d[i][0] + d[i][1];
+  if (s == 12345.0) out[0] = s;
+}
+__global__ void k_rate_dfma(int iters, double *out) {
+  const int lane = threadIdx.x & 31;
+  double a = 1.0 + lane * 1e-3, b = 1.0 - lane * 1e-3;
+  double d[8];
+#pragma unroll
+  for (int i = 0; i < 8; i++) d[i] = i;
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int i = 0; i < 8; i++) d[i] = fma(a, b, d[i]);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; i++) s += d[i];
+  if (s == 12345.0) out[0] = s;
+}
+}  // namespace jh
+
+// FMAs executed = ctas * threads/32 * iters * 8 * (256 for DMMA, 32 for DFMA)
+extern "C" int jh_probe_rate(int kind, int ctas, int threads, int iters, double *out,
+                             void *stream) {
+  if (kind == 0)
+    jh::k_rate_dmma<<<ctas, threads, 0, (cudaStream_t)stream>>>(iters, out);
+  else
+    jh::k_rate_dfma<<<ctas, threads, 0, (cudaStream_t)stream>>>(iters, out);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : -(int)e;
+}

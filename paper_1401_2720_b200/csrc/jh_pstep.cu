@@ -272,6 +272,205 @@ __device__ InnerOut cta_inner_jacobi(double *R, double *V, int w, const int32_t 
   return out;
 }
 
+// Low-latency variant used by the fused path: the dot products and rotation
+// parameters of all w/2 pairs of an inner p-step are formed by w/2 lanes of
+// warp 0 at once (lane = pair; each lane runs the reference's three in-order
+// fma chains over the w rows of its two columns), published in shared
+// memory, and applied by all threads (one (pair, row) item per thread and
+// matrix).  R and V live in shared memory with column stride w + 1, which
+// keeps the lanes' column reads nearly conflict free.  Two CTA barriers per
+// inner p-step.
+struct Inner2Shared {
+  double cs[kMaxW / 2], tn[kMaxW / 2];
+  int act[kMaxW / 2];   // 0 skip, 1 rotate, 2 rotate + swap; bit 2 = hyperbolic
+  int fail_status, fail_bad, stop;
+  int sweep_rot, sweep_proper;
+};
+
+__device__ InnerOut cta_inner_jacobi2(double *R, double *V, int w, int ld,
+                                      const int32_t *__restrict__ steps, const int8_t *sg,
+                                      double tol_c, int max_sweeps, Inner2Shared *sh) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int half = w / 2;
+  InnerOut out{0, 0, 0, 0, -1};
+  for (int sw = 0; sw < max_sweeps; sw++) {
+    int a_r = 0, b_r = 0;  // per lane of warp 0
+    for (int si = 0; si < w - 1; si++) {
+      const int32_t *st = steps + (size_t)si * half * 2;
+      if (warp == 0) {
+        int act = 0, fail = 0, bad = 0;
+        double cs = 1.0, tn = 0.0;
+        if (lane < half) {
+          const int p = st[2 * lane], q = st[2 * lane + 1];
+          const double *cp = R + p * ld, *cq = R + q * ld;
+          double hpp = 0.0, hqq = 0.0, hpq = 0.0;
+#pragma unroll 8
+          for (int i = 0; i < w; i++) {
+            const double gp = cp[i], gq = cq[i];
+            hpp = fma(gp, gp, hpp);
+            hqq = fma(gq, gq, hqq);
+            hpq = fma(gp, gq, hpq);
+          }
+          if (hpp == 0.0) {
+            fail = kZeroColumn;
+            bad = p + 1;
+          } else if (hqq == 0.0) {
+            fail = kZeroColumn;
+            bad = q + 1;
+          } else if (!(fabs(hpq) < tol_c * sqrt(hpp) * sqrt(hqq))) {
+            const bool hyp = sg[p] > 0 && sg[q] < 0;
+            if (!rotation_core(hpp, hqq, hpq, hyp ? -1.0 : 1.0, cs, tn)) {
+              fail = kHypDomain;
+              bad = p + 1;
+            } else {
+              a_r++;
+              if (cs != 1.0) b_r++;
+              act = 1;
+              if (hyp) {
+                act |= 4;
+              } else {
+                const double h1 = fma(-tn, hpq, hpp);
+                const double h2 = fma(tn, hpq, hqq);
+                if ((sg[p] > 0 && h1 < h2) || (sg[p] < 0 && h1 > h2)) act = 2;
+              }
+            }
+          }
+          sh->act[lane] = act;
+          sh->cs[lane] = cs;
+          sh->tn[lane] = tn;
+        }
+        const unsigned fm = __ballot_sync(0xffffffffu, fail != 0);
+        if (lane == 0) sh->stop = 0;
+        if (fm) {
+          const int first = __ffs(fm) - 1;  // first failing pair in reference order
+          const int fs = __shfl_sync(0xffffffffu, fail, first);
+          const int fb = __shfl_sync(0xffffffffu, bad, first);
+          if (lane == 0) {
+            sh->fail_status = fs;
+            sh->fail_bad = fb;
+            sh->stop = 1;
+          }
+        }
+      }
+      __syncthreads();
+      if (sh->stop) {
+        out.status = sh->fail_status;
+        out.bad = sh->fail_bad;
+        out.sweeps = sw;
+        return out;
+      }
+      // apply: item = (pair, row)
+      for (int it = threadIdx.x; it < half * w; it += blockDim.x) {
+        const int pi = it / w, i = it - pi * w;
+        const int act = sh->act[pi];
+        if (!(act & 3)) continue;
+        const int p = st[2 * pi], q = st[2 * pi + 1];
+        const double cs = sh->cs[pi], tn = sh->tn[pi];
+        const double s = (act & 4) ? tn : -tn;
+        double *rp = R + p * ld + i, *rq = R + q * ld + i;
+        double *vp = V + p * ld + i, *vq = V + q * ld + i;
+        const double gp = *rp, gq = *rq, xp = *vp, xq = *vq;
+        double np = fma(s, gq, gp), nq = fma(tn, gp, gq);
+        double mp = fma(s, xq, xp), mq = fma(tn, xp, xq);
+        if (cs != 1.0) {
+          np = np * cs;
+          nq = nq * cs;
+          mp = mp * cs;
+          mq = mq * cs;
+        }
+        if ((act & 3) == 2) {
+          *rp = nq; *rq = np; *vp = mq; *vq = mp;
+        } else {
+          *rp = np; *rq = nq; *vp = mp; *vq = mq;
+        }
+      }
+      __syncthreads();
+    }
+    // sweep end
+    if (warp == 0) {
+      const int ta = __reduce_add_sync(0xffffffffu, a_r);
+      const int tb = __reduce_add_sync(0xffffffffu, b_r);
+      if (lane == 0) {
+        sh->sweep_rot = ta;
+        sh->sweep_proper = tb;
+      }
+    }
+    __syncthreads();
+    const int ta = sh->sweep_rot, tb = sh->sweep_proper;
+    __syncthreads();
+    out.sweeps++;
+    out.rot += ta;
+    out.proper += tb;
+    if (ta == 0) break;
+  }
+  return out;
+}
+
+// K2 (fast): Cholesky + inner Jacobi, one CTA of kInnerThreads per task.
+constexpr int kInnerThreads = 128;
+
+__global__ void __launch_bounds__(kInnerThreads)
+k_factor_inner2(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
+                int64_t *__restrict__ task_rot, const int32_t *__restrict__ pairs, int bw,
+                int64_t n_plus, const int32_t *__restrict__ inner, int inner_limit,
+                double tol_c, unsigned long long *counters, int pstep) {
+  const int w = 2 * bw, ld = w + 1;
+  const int task = blockIdx.x;
+  const int p = pairs[2 * task], q = pairs[2 * task + 1];
+  extern __shared__ double sm[];
+  double *H = sm;            // w x w, ld w (Cholesky), then R with ld w+1 in Rm
+  double *Rm = sm + w * w;   // w x (w+1)
+  double *V = Rm + w * ld;   // w x (w+1)
+  __shared__ int8_t sg[kMaxW];
+  __shared__ Inner2Shared sh;
+  __shared__ int s_status;
+  const double *Hg = Hbuf + (int64_t)task * w * w;
+  for (int i = threadIdx.x; i < w * w; i += blockDim.x) H[i] = Hg[i];
+  for (int i = threadIdx.x; i < w * ld; i += blockDim.x) {
+    const int col = i / ld, row = i - col * ld;
+    V[i] = (row == col) ? 1.0 : 0.0;
+  }
+  for (int j = threadIdx.x; j < w; j += blockDim.x) {
+    const int64_t gcol = (j < bw ? (int64_t)p * bw + j : (int64_t)q * bw + (j - bw)) + 1;
+    sg[j] = gcol <= n_plus ? 1 : -1;
+  }
+  if (threadIdx.x == 0) s_status = 0;
+  __syncthreads();
+  const int info = cta_cholesky(H, w, &s_status);
+  if (info) {
+    if (threadIdx.x == 0) {
+      task_rot[task] = 0;
+      atomicMin(&counters[2], err_key(pstep, task, kCholesky, info));
+    }
+    return;
+  }
+  // R = L^T: R[i][j] = L[j][i] = H[i*w + j] for i <= j, 0 below
+  for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
+    const int j = e / w, i = e - j * w;
+    Rm[j * ld + i] = (i <= j) ? H[i * w + j] : 0.0;
+  }
+  __syncthreads();
+  const InnerOut o = cta_inner_jacobi2(Rm, V, w, ld, inner, sg, tol_c, inner_limit, &sh);
+  if (o.status) {
+    if (threadIdx.x == 0) {
+      task_rot[task] = 0;
+      atomicMin(&counters[2], err_key(pstep, task, o.status, o.bad));
+    }
+    return;
+  }
+  double *Vg = Vbuf + (int64_t)task * w * w;
+  for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
+    const int j = e / w, i = e - j * w;
+    Vg[e] = V[j * ld + i];
+  }
+  if (threadIdx.x == 0) {
+    task_rot[task] = o.rot;
+    atomicAdd(&counters[0], (unsigned long long)o.rot);
+    atomicAdd(&counters[1], (unsigned long long)o.proper);
+    if (o.rot) atomicAdd(&counters[3], 1ull);
+  }
+}
+
 // K2: Cholesky + inner Jacobi for every task of the p-step; one CTA of
 // 32 * max(1, w/2) threads per task.  Dynamic smem: H/R and V (2 w^2 doubles).
 //   counters[0] += rotations, counters[1] += proper rotations,
@@ -531,6 +730,7 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
   const int nbv = V ? (int)cdiv(nv, kUpdRows) : 0;
   const size_t smem_gram = sizeof(double) * kGramChunk * w;
   const size_t smem_inner = sizeof(double) * 2 * (size_t)w * w;
+  const size_t smem_inner2 = sizeof(double) * ((size_t)w * w + 2 * (size_t)w * (w + 1));
   const size_t smem_upd = sizeof(double) * ((size_t)w * w + (size_t)w * kUpdRows);
   static bool attr_set = false;
   if (!attr_set) {
@@ -538,6 +738,8 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
                          (int)(sizeof(double) * (kMaxW * kMaxW + kMaxW * kUpdRows)));
     cudaFuncSetAttribute(k_factor_inner, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(sizeof(double) * 2 * kMaxW * kMaxW));
+    cudaFuncSetAttribute(k_factor_inner2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(double) * (kMaxW * kMaxW + 2 * kMaxW * (kMaxW + 1))));
     attr_set = true;
   }
   // fast paths (DMMA tiles) unless JHSVD_FORCE_SIMPLE is set (parity tests)
@@ -553,8 +755,12 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
       k_gram<<<ntask, kGramThreads, smem_gram, st>>>(G, ldg, m, pairs, bw, Hbuf);
     prof_mark(st, 0, true);
     prof_mark(st, 1, false);
-    k_factor_inner<<<ntask, thr_inner, smem_inner, st>>>(Hbuf, Vbuf, trot, pairs, bw, n_plus, inner,
-                                                 inner_limit, tol_c, counters, s);
+    if (force_simple)
+      k_factor_inner<<<ntask, thr_inner, smem_inner, st>>>(Hbuf, Vbuf, trot, pairs, bw, n_plus,
+                                                           inner, inner_limit, tol_c, counters, s);
+    else
+      k_factor_inner2<<<ntask, kInnerThreads, smem_inner2, st>>>(
+          Hbuf, Vbuf, trot, pairs, bw, n_plus, inner, inner_limit, tol_c, counters, s);
     prof_mark(st, 1, true);
     dim3 grid(ntask, nbg + nbv);
     prof_mark(st, 2, false);

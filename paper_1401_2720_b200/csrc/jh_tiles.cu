@@ -13,6 +13,8 @@
 #include "jh_dmma.cuh"
 #include "jh_kernels.h"
 
+#include <cstdlib>
+
 namespace jh {
 
 // ---------------------------------------------------------------------------
@@ -31,21 +33,83 @@ constexpr int kRch = 64;          // rows per staged chunk
 constexpr int kLd = kRch + 4;     // padded smem column stride (doubles)
 constexpr int kStages = 3;
 
-template <int W>
-__global__ void __launch_bounds__(32)
+// Consumer side of the Gram for warp WARP of NW: it owns tiles i = WARP
+// (mod NW) of the (W/8)(W/8+1)/2 lower tiles (enumerated row-major, X >= Y).
+template <int W, int NW>
+struct GramTiles {
+  static constexpr int NT = W / 8;
+  static constexpr int NTILE = NT * (NT + 1) / 2;
+  static constexpr int MY = (NTILE + NW - 1) / NW;
+};
+
+template <int W, int NW, int WARP>
+__device__ __forceinline__ void gram_chunk(const double *buf, int nr, double (&acc)[GramTiles<W, NW>::MY][2],
+                                           int t) {
+  constexpr int NT = W / 8;
+  auto step = [&](int kk, bool guard) {
+    double f[NT];
+    const bool ok = !guard || (4 * kk + t < nr);
+#pragma unroll
+    for (int X = 0; X < NT; X++) f[X] = ok ? buf[X * 8 * kLd + 4 * kk] : 0.0;
+    int i = 0, mine = 0;
+#pragma unroll
+    for (int X = 0; X < NT; X++)
+#pragma unroll
+      for (int Y = 0; Y <= X; Y++, i++)
+        if (i % NW == WARP) {
+          dmma(acc[mine][0], acc[mine][1], f[X], f[Y]);
+          mine++;
+        }
+  };
+  if (nr == kRch) {
+#pragma unroll 4
+    for (int kk = 0; kk < kRch / 4; kk++) step(kk, false);
+  } else {
+    const int nks = (nr + 3) / 4;
+    for (int kk = 0; kk < nks; kk++) step(kk, true);
+  }
+}
+
+template <int W, int NW, int WARP>
+__device__ __forceinline__ void gram_store(double *H, const double (&acc)[GramTiles<W, NW>::MY][2],
+                                           int g, int t) {
+  constexpr int NT = W / 8;
+  int i = 0, mine = 0;
+#pragma unroll
+  for (int X = 0; X < NT; X++)
+#pragma unroll
+    for (int Y = 0; Y <= X; Y++, i++)
+      if (i % NW == WARP) {
+#pragma unroll
+        for (int j = 0; j < 2; j++) {
+          const int x = 8 * X + g, y = 8 * Y + 2 * t + j;
+          H[y * W + x] = acc[mine][j];
+          if (X != Y) H[x * W + y] = acc[mine][j];
+        }
+        mine++;
+      }
+}
+
+template <int W, int NW>
+__global__ void __launch_bounds__(32 * NW)
 k_gram_tma(const double *__restrict__ G, int64_t ldg, int64_t m,
            const int32_t *__restrict__ pairs, double *__restrict__ Hbuf) {
-  constexpr int NT = W / 8, BW = W / 2, NTILE = NT * (NT + 1) / 2;
+  constexpr int BW = W / 2, MY = GramTiles<W, NW>::MY;
   extern __shared__ __align__(128) double sm[];  // [kStages][W][kLd]
-  __shared__ __align__(8) uint64_t full[kStages];
-  const int task = blockIdx.x, lane = threadIdx.x, g = lane >> 2, t = lane & 3;
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  const int task = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
   const int p = pairs[2 * task], q = pairs[2 * task + 1];
   const int64_t nchunk = cdiv(m, kRch);
-  if (lane == 0) {
-    for (int s = 0; s < kStages; s++) mbar_init(&full[s], 1);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
     fence_mbar_init();
   }
-  __syncwarp();
+  __syncthreads();
+  // warp 0 issues the copies of chunk c (one column per lane)
   auto issue = [&](int64_t c) {
     const int s = (int)(c % kStages);
     const int64_t r0 = c * kRch;
@@ -57,58 +121,35 @@ k_gram_tma(const double *__restrict__ G, int64_t ldg, int64_t m,
       bulk_g2s(sm + ((size_t)s * W + j) * kLd, G + col * ldg + r0, bytes, &full[s]);
     }
   };
-  for (int64_t c = 0; c < kStages && c < nchunk; c++) issue(c);
+  if (warp == 0)
+    for (int64_t c = 0; c < kStages && c < nchunk; c++) issue(c);
 
-  double acc[NTILE][2];
+  double acc[MY][2];
 #pragma unroll
-  for (int i = 0; i < NTILE; i++) acc[i][0] = acc[i][1] = 0.0;
+  for (int i = 0; i < MY; i++) acc[i][0] = acc[i][1] = 0.0;
 
   for (int64_t c = 0; c < nchunk; c++) {
     const int s = (int)(c % kStages);
-    mbar_wait(&full[s], (uint32_t)((c / kStages) & 1));
+    const uint32_t ph = (uint32_t)((c / kStages) & 1);
+    mbar_wait(&full[s], ph);
     const double *buf = sm + (size_t)s * W * kLd + (size_t)g * kLd + t;
     const int nr = (int)min64(kRch, m - c * kRch);
-    if (nr == kRch) {
-#pragma unroll 4
-      for (int kk = 0; kk < kRch / 4; kk++) {
-        double f[NT];
-#pragma unroll
-        for (int X = 0; X < NT; X++) f[X] = buf[X * 8 * kLd + 4 * kk];
-        int i = 0;
-#pragma unroll
-        for (int X = 0; X < NT; X++)
-#pragma unroll
-          for (int Y = 0; Y <= X; Y++, i++) dmma(acc[i][0], acc[i][1], f[X], f[Y]);
-      }
-    } else {
-      const int nks = (nr + 3) / 4;
-      for (int kk = 0; kk < nks; kk++) {
-        const bool ok = 4 * kk + t < nr;
-        double f[NT];
-#pragma unroll
-        for (int X = 0; X < NT; X++) f[X] = ok ? buf[X * 8 * kLd + 4 * kk] : 0.0;
-        int i = 0;
-#pragma unroll
-        for (int X = 0; X < NT; X++)
-#pragma unroll
-          for (int Y = 0; Y <= X; Y++, i++) dmma(acc[i][0], acc[i][1], f[X], f[Y]);
-      }
-    }
+    if (warp == 0)
+      gram_chunk<W, NW, 0>(buf, nr, acc, t);
+    else if (NW > 1 && warp == 1)
+      gram_chunk<W, NW, (NW > 1 ? 1 : 0)>(buf, nr, acc, t);
     __syncwarp();
-    if (c + kStages < nchunk) issue(c + kStages);
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (warp == 0 && c + kStages < nchunk) {
+      mbar_wait(&empty[s], ph);
+      issue(c + kStages);
+    }
   }
   double *H = Hbuf + (size_t)task * W * W;  // column-major: H[y * W + x] = h[x][y]
-  int i = 0;
-#pragma unroll
-  for (int X = 0; X < NT; X++)
-#pragma unroll
-    for (int Y = 0; Y <= X; Y++, i++)
-#pragma unroll
-      for (int j = 0; j < 2; j++) {
-        const int x = 8 * X + g, y = 8 * Y + 2 * t + j;
-        H[y * W + x] = acc[i][j];
-        if (X != Y) H[x * W + y] = acc[i][j];
-      }
+  if (warp == 0)
+    gram_store<W, NW, 0>(H, acc, g, t);
+  else if (NW > 1 && warp == 1)
+    gram_store<W, NW, (NW > 1 ? 1 : 0)>(H, acc, g, t);
 }
 
 // ---------------------------------------------------------------------------
@@ -202,6 +243,109 @@ k_update_dmma(double *__restrict__ G, int64_t ldg, int64_t m, double *__restrict
   }
 }
 
+// K3 (TMA variant): the same post-multiplication with the pair rows streamed
+// through a 4-stage shared-memory ring by the TMA engine, so the bytes in
+// flight do not cost registers.  Warp 0 produces (one 512 B bulk copy per
+// column and chunk of 64 rows); warps 1..4 consume 16 rows each per chunk
+// (two 8-row DMMA blocks, A fragments by conflict-free LDS.64 from the
+// padded ring, V' fragments in registers) and store the results straight to
+// global memory (whole 32 B sectors).  A CTA owns a slab of kUpdSlab rows of
+// one matrix for one task.
+
+constexpr int kUpdStages = 4;
+constexpr int kUpdCons = 4;        // consumer warps
+constexpr int kUpdSlab = 2048;     // rows per CTA
+
+template <int W>
+__global__ void __launch_bounds__(32 * (kUpdCons + 1))
+k_update_tma(double *__restrict__ G, int64_t ldg, int64_t m, double *__restrict__ V,
+             int64_t ldv, int64_t nv, const int32_t *__restrict__ pairs,
+             const double *__restrict__ Vbuf, const int64_t *__restrict__ trot, int nslab_g) {
+  constexpr int NT = W / 8, NK = W / 4, BW = W / 2;
+  extern __shared__ __align__(128) double ring[];  // [kUpdStages][W][kLd]
+  __shared__ __align__(8) uint64_t full[kUpdStages], empty[kUpdStages];
+  const int task = blockIdx.x;
+  if (trot[task] == 0) return;
+  const int p = pairs[2 * task], q = pairs[2 * task + 1];
+  double *A;
+  int64_t ld, rows, s0;
+  if ((int)blockIdx.y < nslab_g) {
+    A = G; ld = ldg; rows = m; s0 = (int64_t)blockIdx.y * kUpdSlab;
+  } else {
+    A = V; ld = ldv; rows = nv; s0 = (int64_t)(blockIdx.y - nslab_g) * kUpdSlab;
+  }
+  const int64_t s1 = min64(s0 + kUpdSlab, rows);
+  const int nchunk = (int)cdiv(s1 - s0, kRch);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kUpdStages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kUpdCons);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == 0) {
+    // producer
+    for (int c = 0; c < nchunk; c++) {
+      const int s = c % kUpdStages;
+      if (c >= kUpdStages) mbar_wait(&empty[s], (uint32_t)(((c / kUpdStages) - 1) & 1));
+      const int64_t r0 = s0 + (int64_t)c * kRch;
+      const uint32_t bytes = (uint32_t)min64(kRch, s1 - r0) * 8u;
+      if (lane == 0) mbar_expect_tx(&full[s], bytes * W);
+      __syncwarp();
+      for (int j = lane; j < W; j += 32) {
+        const int64_t col = j < BW ? (int64_t)p * BW + j : (int64_t)q * BW + (j - BW);
+        bulk_g2s(ring + ((size_t)s * W + j) * kLd, A + col * ld + r0, bytes, &full[s]);
+      }
+    }
+    return;
+  }
+  // consumers
+  const int cw = warp - 1;
+  const double *Vt = Vbuf + (size_t)task * W * W;
+  double bf[NK][NT];
+#pragma unroll
+  for (int kk = 0; kk < NK; kk++)
+#pragma unroll
+    for (int Y = 0; Y < NT; Y++) bf[kk][Y] = Vt[(8 * Y + g) * W + 4 * kk + t];
+  double *pout = A + ((int64_t)p * BW + 2 * t) * ld;
+  double *qout = A + ((int64_t)q * BW + 2 * t) * ld;
+  for (int c = 0; c < nchunk; c++) {
+    const int s = c % kUpdStages;
+    mbar_wait(&full[s], (uint32_t)((c / kUpdStages) & 1));
+    const int64_t r0 = s0 + (int64_t)c * kRch;
+    const double *buf = ring + (size_t)s * W * kLd;
+#pragma unroll
+    for (int rb = 0; rb < 2; rb++) {
+      const int rl = cw * 16 + rb * 8;
+      double a[NK];
+#pragma unroll
+      for (int kk = 0; kk < NK; kk++) a[kk] = buf[(4 * kk + t) * kLd + rl + g];
+      double acc[NT][2];
+#pragma unroll
+      for (int Y = 0; Y < NT; Y++) acc[Y][0] = acc[Y][1] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < NK; kk++)
+#pragma unroll
+        for (int Y = 0; Y < NT; Y++) dmma(acc[Y][0], acc[Y][1], a[kk], bf[kk][Y]);
+      const int64_t row = r0 + rl + g;
+      if (row < s1) {
+#pragma unroll
+        for (int Y = 0; Y < NT; Y++)
+#pragma unroll
+          for (int j = 0; j < 2; j++) {
+            double *dst = Y < NT / 2 ? pout + (int64_t)(8 * Y + j) * ld
+                                     : qout + (int64_t)(8 * Y + j - BW) * ld;
+            st_f64(dst + row, acc[Y][j]);
+          }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host launchers
 
@@ -209,16 +353,19 @@ bool gram_tma_ok(int w, int64_t m, int64_t ldg) {
   return (w == 16 || w == 32) && m % 2 == 0 && ldg % 2 == 0;
 }
 
+constexpr int kGramWarps = 2;
+
 template <int W>
 static void launch_gram_t(const double *G, int64_t ldg, int64_t m, const int32_t *pairs,
                           int ntask, double *Hbuf, cudaStream_t st) {
   const size_t smem = sizeof(double) * (size_t)kStages * W * kLd;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_gram_tma<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_gram_tma<W, kGramWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
     attr = true;
   }
-  k_gram_tma<W><<<ntask, 32, smem, st>>>(G, ldg, m, pairs, Hbuf);
+  k_gram_tma<W, kGramWarps><<<ntask, 32 * kGramWarps, smem, st>>>(G, ldg, m, pairs, Hbuf);
 }
 
 void launch_gram_tma(const double *G, int64_t ldg, int64_t m, const int32_t *pairs, int ntask,
@@ -231,9 +378,37 @@ void launch_gram_tma(const double *G, int64_t ldg, int64_t m, const int32_t *pai
 
 bool update_dmma_ok(int w) { return w == 16 || w == 32; }
 
+template <int W>
+static void launch_update_tma_t(double *G, int64_t ldg, int64_t m, double *V, int64_t ldv,
+                                int64_t nv, const int32_t *pairs, int ntask, const double *Vbuf,
+                                const int64_t *trot, cudaStream_t st) {
+  const size_t smem = sizeof(double) * (size_t)kUpdStages * W * kLd;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_update_tma<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr = true;
+  }
+  const int nsg = (int)cdiv(m, kUpdSlab);
+  const int nsv = V ? (int)cdiv(nv, kUpdSlab) : 0;
+  dim3 grid(ntask, nsg + nsv);
+  k_update_tma<W><<<grid, 32 * (kUpdCons + 1), smem, st>>>(G, ldg, m, V, ldv, nv, pairs, Vbuf,
+                                                          trot, nsg);
+}
+
 void launch_update_dmma(double *G, int64_t ldg, int64_t m, double *V, int64_t ldv, int64_t nv,
                         const int32_t *pairs, int ntask, int w, const double *Vbuf,
                         const int64_t *trot, cudaStream_t st) {
+  static const char *mode = getenv("JHSVD_UPDATE");  // "ldg" selects the LDG variant
+  const bool tma = !(mode && mode[0] == 'l') && m % 2 == 0 && ldg % 2 == 0 &&
+                   (!V || (nv % 2 == 0 && ldv % 2 == 0));
+  if (tma) {
+    if (w == 16)
+      launch_update_tma_t<16>(G, ldg, m, V, ldv, nv, pairs, ntask, Vbuf, trot, st);
+    else
+      launch_update_tma_t<32>(G, ldg, m, V, ldv, nv, pairs, ntask, Vbuf, trot, st);
+    return;
+  }
   const int64_t slab = (int64_t)kUpdWarps * kUpdRpw;
   const int nsg = (int)cdiv(m, slab);
   const int nsv = V ? (int)cdiv(nv, slab) : 0;

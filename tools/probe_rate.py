@@ -1,0 +1,38 @@
+"""Measure sustained FP64 DMMA and DFMA rates on this GPU (dev tool)."""
+import json
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_1401_2720_b200 import _lib  # noqa: E402
+
+
+def main():
+    lib = _lib.require_cuda()
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    res = []
+    for kind, name, per in ((0, "dmma", 256), (1, "dfma", 32)):
+        for wps in (1, 2, 4, 8, 16, 32):
+            iters = 20000 if kind == 0 else 100000
+            ctas = sms * max(1, wps // 4)
+            threads = 32 * min(wps, 4)
+            for rep in range(2):
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                _lib.check(lib.jh_probe_rate(kind, ctas, threads, iters, out.data_ptr(),
+                                             _lib.stream_handle()), "rate")
+                e1.record()
+                torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            fma = ctas * threads / 32 * iters * 8 * per
+            r = {"kind": name, "warps_per_sm": wps, "tflops": 2 * fma / ms / 1e9}
+            print(json.dumps(r), flush=True)
+            res.append(r)
+    return res
+
+
+if __name__ == "__main__":
+    main()
