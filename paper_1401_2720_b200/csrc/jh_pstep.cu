@@ -758,6 +758,9 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
     if (force_simple)
       k_factor_inner<<<ntask, thr_inner, smem_inner, st>>>(Hbuf, Vbuf, trot, pairs, bw, n_plus,
                                                            inner, inner_limit, tol_c, counters, s);
+    else if (inner3_ok(w))
+      launch_inner3(Hbuf, Vbuf, trot, pairs, ntask, w, n_plus, inner, inner_limit, tol_c,
+                    counters, s, st);
     else
       k_factor_inner2<<<ntask, kInnerThreads, smem_inner2, st>>>(
           Hbuf, Vbuf, trot, pairs, bw, n_plus, inner, inner_limit, tol_c, counters, s);

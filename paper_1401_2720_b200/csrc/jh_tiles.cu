@@ -46,11 +46,7 @@ template <int W, int NW, int WARP>
 __device__ __forceinline__ void gram_chunk(const double *buf, int nr, double (&acc)[GramTiles<W, NW>::MY][2],
                                            int t) {
   constexpr int NT = W / 8;
-  auto step = [&](int kk, bool guard) {
-    double f[NT];
-    const bool ok = !guard || (4 * kk + t < nr);
-#pragma unroll
-    for (int X = 0; X < NT; X++) f[X] = ok ? buf[X * 8 * kLd + 4 * kk] : 0.0;
+  auto tiles = [&](const double (&f)[NT]) {
     int i = 0, mine = 0;
 #pragma unroll
     for (int X = 0; X < NT; X++)
@@ -61,9 +57,30 @@ __device__ __forceinline__ void gram_chunk(const double *buf, int nr, double (&a
           mine++;
         }
   };
+  auto step = [&](int kk, bool guard) {
+    double f[NT];
+    const bool ok = !guard || (4 * kk + t < nr);
+#pragma unroll
+    for (int X = 0; X < NT; X++) f[X] = ok ? buf[X * 8 * kLd + 4 * kk] : 0.0;
+    tiles(f);
+  };
   if (nr == kRch) {
-#pragma unroll 4
-    for (int kk = 0; kk < kRch / 4; kk++) step(kk, false);
+    // explicit two-stage register pipeline: fragments of k-step kk+1 are
+    // loaded before the DMMAs of k-step kk are issued
+    double fa[NT], fb[NT];
+#pragma unroll
+    for (int X = 0; X < NT; X++) fa[X] = buf[X * 8 * kLd];
+#pragma unroll
+    for (int kk = 0; kk < kRch / 4; kk += 2) {
+#pragma unroll
+      for (int X = 0; X < NT; X++) fb[X] = buf[X * 8 * kLd + 4 * (kk + 1)];
+      tiles(fa);
+      if (kk + 2 < kRch / 4) {
+#pragma unroll
+        for (int X = 0; X < NT; X++) fa[X] = buf[X * 8 * kLd + 4 * (kk + 2)];
+      }
+      tiles(fb);
+    }
   } else {
     const int nks = (nr + 3) / 4;
     for (int kk = 0; kk < nks; kk++) step(kk, true);
@@ -91,9 +108,10 @@ __device__ __forceinline__ void gram_store(double *H, const double (&acc)[GramTi
 }
 
 template <int W, int NW>
-__global__ void __launch_bounds__(32 * NW)
+__global__ void __launch_bounds__(32 * (NW + 1))
 k_gram_tma(const double *__restrict__ G, int64_t ldg, int64_t m,
            const int32_t *__restrict__ pairs, double *__restrict__ Hbuf) {
+  // warp 0 produces (TMA bulk copies), warps 1..NW consume (DMMA)
   constexpr int BW = W / 2, MY = GramTiles<W, NW>::MY;
   extern __shared__ __align__(128) double sm[];  // [kStages][W][kLd]
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
@@ -109,46 +127,42 @@ k_gram_tma(const double *__restrict__ G, int64_t ldg, int64_t m,
     fence_mbar_init();
   }
   __syncthreads();
-  // warp 0 issues the copies of chunk c (one column per lane)
-  auto issue = [&](int64_t c) {
-    const int s = (int)(c % kStages);
-    const int64_t r0 = c * kRch;
-    const uint32_t bytes = (uint32_t)min64(kRch, m - r0) * 8u;
-    if (lane == 0) mbar_expect_tx(&full[s], bytes * W);
-    __syncwarp();
-    for (int j = lane; j < W; j += 32) {
-      const int64_t col = j < BW ? (int64_t)p * BW + j : (int64_t)q * BW + (j - BW);
-      bulk_g2s(sm + ((size_t)s * W + j) * kLd, G + col * ldg + r0, bytes, &full[s]);
+  if (warp == 0) {
+    for (int64_t c = 0; c < nchunk; c++) {
+      const int s = (int)(c % kStages);
+      if (c >= kStages) mbar_wait(&empty[s], (uint32_t)(((c / kStages) - 1) & 1));
+      const int64_t r0 = c * kRch;
+      const uint32_t bytes = (uint32_t)min64(kRch, m - r0) * 8u;
+      if (lane == 0) mbar_expect_tx(&full[s], bytes * W);
+      __syncwarp();
+      for (int j = lane; j < W; j += 32) {
+        const int64_t col = j < BW ? (int64_t)p * BW + j : (int64_t)q * BW + (j - BW);
+        bulk_g2s(sm + ((size_t)s * W + j) * kLd, G + col * ldg + r0, bytes, &full[s]);
+      }
     }
-  };
-  if (warp == 0)
-    for (int64_t c = 0; c < kStages && c < nchunk; c++) issue(c);
-
+    return;
+  }
+  const int cw = warp - 1;
   double acc[MY][2];
 #pragma unroll
   for (int i = 0; i < MY; i++) acc[i][0] = acc[i][1] = 0.0;
 
   for (int64_t c = 0; c < nchunk; c++) {
     const int s = (int)(c % kStages);
-    const uint32_t ph = (uint32_t)((c / kStages) & 1);
-    mbar_wait(&full[s], ph);
+    mbar_wait(&full[s], (uint32_t)((c / kStages) & 1));
     const double *buf = sm + (size_t)s * W * kLd + (size_t)g * kLd + t;
     const int nr = (int)min64(kRch, m - c * kRch);
-    if (warp == 0)
+    if (cw == 0)
       gram_chunk<W, NW, 0>(buf, nr, acc, t);
-    else if (NW > 1 && warp == 1)
+    else if (NW > 1 && cw == 1)
       gram_chunk<W, NW, (NW > 1 ? 1 : 0)>(buf, nr, acc, t);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
-    if (warp == 0 && c + kStages < nchunk) {
-      mbar_wait(&empty[s], ph);
-      issue(c + kStages);
-    }
   }
   double *H = Hbuf + (size_t)task * W * W;  // column-major: H[y * W + x] = h[x][y]
-  if (warp == 0)
+  if (cw == 0)
     gram_store<W, NW, 0>(H, acc, g, t);
-  else if (NW > 1 && warp == 1)
+  else if (NW > 1 && cw == 1)
     gram_store<W, NW, (NW > 1 ? 1 : 0)>(H, acc, g, t);
 }
 
@@ -365,7 +379,8 @@ static void launch_gram_t(const double *G, int64_t ldg, int64_t m, const int32_t
                          (int)smem);
     attr = true;
   }
-  k_gram_tma<W, kGramWarps><<<ntask, 32 * kGramWarps, smem, st>>>(G, ldg, m, pairs, Hbuf);
+  k_gram_tma<W, kGramWarps><<<ntask, 32 * (kGramWarps + 1), smem, st>>>(G, ldg, m, pairs,
+                                                                       Hbuf);
 }
 
 void launch_gram_tma(const double *G, int64_t ldg, int64_t m, const int32_t *pairs, int ntask,
