@@ -111,6 +111,10 @@ int jh_probe_dmma(const double *A, const double *B, const double *C, double *Dm,
  * runs 8 independent chains for `iters` iterations. */
 int jh_probe_rate(int kind, int ctas, int threads, int iters, double *out, void *stream);
 
+/* Diagnostic: dependent-chain latencies (cycles/op) of DFMA, DMUL, division,
+ * sqrt, the rotation formula and a shared-memory load; out[6]. */
+int jh_probe_latency(double *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -155,6 +155,12 @@ k_factor_inner3(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
             hpq = fma(gp, gq, hpq);
           }
           StepParams pr{1.0, 0.0, 0};
+          // the rotation is formed speculatively, in parallel with the
+          // orthogonality test (it has no side effects; a pair that passes
+          // the test discards it, exactly like the reference never forms it)
+          const bool hyp = S.sg[p] > 0 && S.sg[q] < 0;
+          double cs, tn;
+          const bool rot_ok = rotation_core(hpp, hqq, hpq, hyp ? -1.0 : 1.0, cs, tn);
           if (hpp == 0.0) {
             fail = kZeroColumn;
             fb = p + 1;
@@ -162,9 +168,7 @@ k_factor_inner3(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
             fail = kZeroColumn;
             fb = q + 1;
           } else if (!(fabs(hpq) < tol_c * sqrt(hpp) * sqrt(hqq))) {
-            const bool hyp = S.sg[p] > 0 && S.sg[q] < 0;
-            double cs, tn;
-            if (!rotation_core(hpp, hqq, hpq, hyp ? -1.0 : 1.0, cs, tn)) {
+            if (!rot_ok) {
               fail = kHypDomain;
               fb = p + 1;
             } else {

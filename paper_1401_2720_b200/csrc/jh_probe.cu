@@ -94,3 +94,55 @@ extern "C" int jh_probe_rate(int kind, int ctas, int threads, int iters, double 
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : -(int)e;
 }
+
+// Diagnostic: single-thread dependent-chain latencies in cycles per op:
+// out[0] DFMA, out[1] DMUL, out[2] division, out[3] sqrt, out[4] rotation_core
+// (trig), out[5] shared-memory load (pointer chase).
+namespace jh {
+__global__ void k_latency(double seed, double *out) {
+  __shared__ int chase[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) chase[i] = (i * 37 + 11) & 255;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const int N = 1024;
+  double x = seed, y = 1.0000001, z = 0.999999;
+  long long t0 = clock64();
+  for (int i = 0; i < N; i++) x = fma(x, y, z);
+  long long t1 = clock64();
+  out[0] = (double)(t1 - t0) / N + 0.0 * x;
+  double w = seed;
+  t0 = clock64();
+  for (int i = 0; i < N; i++) w = w * y;
+  t1 = clock64();
+  out[1] = (double)(t1 - t0) / N + 0.0 * w;
+  double d = seed + 2.0;
+  t0 = clock64();
+  for (int i = 0; i < N; i++) d = 3.0 / d;
+  t1 = clock64();
+  out[2] = (double)(t1 - t0) / N + 0.0 * d;
+  double s = seed + 3.0;
+  t0 = clock64();
+  for (int i = 0; i < N; i++) s = sqrt(s) + 1.0;
+  t1 = clock64();
+  out[3] = (double)(t1 - t0) / N + 0.0 * s;
+  double hpq = 0.3 + seed, cs, tn;
+  t0 = clock64();
+  for (int i = 0; i < N; i++) {
+    rotation_core(1.5, 1.0, hpq, 1.0, cs, tn);
+    hpq = 0.3 + tn * 1e-9;
+  }
+  t1 = clock64();
+  out[4] = (double)(t1 - t0) / N + 0.0 * cs;
+  int idx = (int)seed & 255;
+  t0 = clock64();
+  for (int i = 0; i < N; i++) idx = chase[idx];
+  t1 = clock64();
+  out[5] = (double)(t1 - t0) / N + 0.0 * idx;
+}
+}  // namespace jh
+
+extern "C" int jh_probe_latency(double *out, void *stream) {
+  jh::k_latency<<<1, 32, 0, (cudaStream_t)stream>>>(0.5, out);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : -(int)e;
+}

@@ -34,5 +34,21 @@ def main():
     return res
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--latency" not in sys.argv:
     main()
+
+
+def latency():
+    lib = _lib.require_cuda()
+    out = torch.zeros(6, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        _lib.check(lib.jh_probe_latency(out.data_ptr(), _lib.stream_handle()), "lat")
+        torch.cuda.synchronize()
+    names = ["dfma", "dmul", "ddiv", "dsqrt", "rotation_core", "lds"]
+    r = dict(zip(names, out.cpu().tolist()))
+    print(json.dumps({"latency_cycles": r}))
+    return r
+
+
+if __name__ == "__main__" and "--latency" in sys.argv:
+    latency()
