@@ -124,12 +124,15 @@ class SweepEngine:
         nbytes = int(self.lib.jh_sweep_workspace_bytes(n, w))
         self.ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
         self.counters = torch.empty(4, dtype=torch.int64, device=dev)
+        self.tasks_rotated: list[int] = []
         self.tol_c = EPS * math.sqrt(w) * cfg.eps_factor
 
-    def sweep(self, G, V, first_step: int = 0, nsteps: Optional[int] = None):
+    def sweep(self, G, V, first_step: int = 0, nsteps: Optional[int] = None,
+              n_plus: Optional[int] = None):
         """Enqueue p-steps [first_step, first_step + nsteps) of one block
         sweep on G (n, m) / V (n, nv) column-major tensors; returns the
-        device counter tensor (rotations, proper, error key)."""
+        device counter tensor (rotations, proper, error key, tasks rotated).
+        ``n_plus`` overrides the signature's +1 count for this sweep."""
         self.counters.zero_()
         self.counters[2].fill_(-1)
         ns = self.nsteps - first_step if nsteps is None else nsteps
@@ -137,7 +140,8 @@ class SweepEngine:
             G.data_ptr(), self.m, self.m, self.n,
             V.data_ptr() if V is not None else None, self.nv, self.nv,
             self.w, self.outer_dev.data_ptr(), int(first_step), int(ns),
-            self.inner_dev.data_ptr(), self.n_plus, self.cfg.inner_sweep_limit, self.tol_c,
+            self.inner_dev.data_ptr(), self.n_plus if n_plus is None else int(n_plus),
+            self.cfg.inner_sweep_limit, self.tol_c,
             self.ws.data_ptr(), self.ws.numel(), self.counters.data_ptr(),
             _lib.stream_handle())
         _lib.check(rc, "jh_block_sweep")
@@ -160,17 +164,24 @@ class SweepEngine:
         raise JDefinitenessError(
             f"hyperbolic pivot at local column {index} has |coth 2phi| < 1")
 
-    def run(self, G, V, early_stop: Optional[Callable[[], bool]] = None):
+    def one_sweep(self, G, V, n_plus: Optional[int] = None) -> tuple[int, int]:
+        """One block sweep; returns (rotations, proper) and raises like the
+        reference on numerical failure."""
+        rot, proper, key, nrot = (int(x) for x in self.sweep(G, V, n_plus=n_plus).cpu().tolist())
+        if key != -1:
+            self.raise_error(key)
+        self.tasks_rotated.append(nrot)
+        return rot, proper
+
+    def run(self, G, V, early_stop: Optional[Callable[[], bool]] = None,
+            n_plus: Optional[int] = None):
         """Sweep loop of run_block_jacobi_inplace (driver.py:176-200)."""
         stats: list[tuple[int, int]] = []
         converged = False
         self.tasks_rotated: list[int] = []
         for _ in range(self.cfg.max_block_sweeps):
-            rot, proper, key, nrot = (int(x) for x in self.sweep(G, V).cpu().tolist())
-            if key != -1:
-                self.raise_error(key)
+            rot, proper = self.one_sweep(G, V, n_plus)
             stats.append((rot, proper))
-            self.tasks_rotated.append(nrot)
             if proper == 0:
                 converged = True
                 break
