@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(InnerCfg<W>::NTH)
 k_factor_inner3(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
                 int64_t *__restrict__ task_rot, const int32_t *__restrict__ pairs,
                 int64_t n_plus, const int32_t *__restrict__ inner, int inner_limit,
-                double tol_c, unsigned long long *counters, int pstep) {
+                double tol_c, unsigned long long *counters, int pstep, int task_base) {
   constexpr int HALF = InnerCfg<W>::HALF, LD = InnerCfg<W>::LD, NTH = InnerCfg<W>::NTH;
   constexpr int BW = W / 2, NSTEP = W - 1;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -118,7 +118,7 @@ k_factor_inner3(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
   if (S.chol) {
     if (tid == 0) {
       task_rot[task] = 0;
-      atomicMin(&counters[2], err_key(pstep, task, kCholesky, S.chol));
+      atomicMin(&counters[2], err_key(pstep, task_base + task, kCholesky, S.chol));
     }
     return;
   }
@@ -240,7 +240,7 @@ k_factor_inner3(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
   if (status) {
     if (tid == 0) {
       task_rot[task] = 0;
-      atomicMin(&counters[2], err_key(pstep, task, status, bad));
+      atomicMin(&counters[2], err_key(pstep, task_base + task, status, bad));
     }
     return;
   }
@@ -272,7 +272,7 @@ template <int W>
 static void launch_inner_t(const double *Hbuf, double *Vbuf, int64_t *trot, const int32_t *pairs,
                            int ntask, int64_t n_plus, const int32_t *inner, int inner_limit,
                            double tol_c, unsigned long long *counters, int pstep,
-                           cudaStream_t st) {
+                           cudaStream_t st, int task_base) {
   const size_t smem = sizeof(InnerSmem<W>);
   static bool attr = false;
   if (!attr) {
@@ -281,21 +281,23 @@ static void launch_inner_t(const double *Hbuf, double *Vbuf, int64_t *trot, cons
     attr = true;
   }
   k_factor_inner3<W><<<ntask, InnerCfg<W>::NTH, smem, st>>>(Hbuf, Vbuf, trot, pairs, n_plus, inner,
-                                                           inner_limit, tol_c, counters, pstep);
+                                                           inner_limit, tol_c, counters, pstep,
+                                                           task_base);
 }
 
 void launch_inner3(const double *Hbuf, double *Vbuf, int64_t *trot, const int32_t *pairs,
                    int ntask, int w, int64_t n_plus, const int32_t *inner, int inner_limit,
-                   double tol_c, unsigned long long *counters, int pstep, cudaStream_t st) {
+                   double tol_c, unsigned long long *counters, int pstep, cudaStream_t st,
+                   int task_base) {
   if (w == 16)
     launch_inner_t<16>(Hbuf, Vbuf, trot, pairs, ntask, n_plus, inner, inner_limit, tol_c,
-                       counters, pstep, st);
+                       counters, pstep, st, task_base);
   else if (w == 32)
     launch_inner_t<32>(Hbuf, Vbuf, trot, pairs, ntask, n_plus, inner, inner_limit, tol_c,
-                       counters, pstep, st);
+                       counters, pstep, st, task_base);
   else
     launch_inner_t<64>(Hbuf, Vbuf, trot, pairs, ntask, n_plus, inner, inner_limit, tol_c,
-                       counters, pstep, st);
+                       counters, pstep, st, task_base);
 }
 
 }  // namespace jh

@@ -21,6 +21,7 @@ void launch_update_dmma(double *G, int64_t ldg, int64_t m, double *V, int64_t ld
 bool inner3_ok(int w);
 void launch_inner3(const double *Hbuf, double *Vbuf, int64_t *trot, const int32_t *pairs,
                    int ntask, int w, int64_t n_plus, const int32_t *inner, int inner_limit,
-                   double tol_c, unsigned long long *counters, int pstep, cudaStream_t st);
+                   double tol_c, unsigned long long *counters, int pstep, cudaStream_t st,
+                   int task_base = 0);
 
 }  // namespace jh

@@ -746,6 +746,69 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
   static const bool force_simple = getenv("JHSVD_FORCE_SIMPLE") != nullptr;
   const bool use_tma_gram = !force_simple && gram_tma_ok(w, m, ldg);
   const bool use_dmma_update = !force_simple && update_dmma_ok(w);
+  static const char *env_streams = getenv("JHSVD_STREAMS");
+  const bool split = use_tma_gram && use_dmma_update && inner3_ok(w) && ntask >= 64 &&
+                     !(env_streams && env_streams[0] == '0');
+  if (split) {
+    // Two half-p-steps in flight: the latency-bound inner Jacobi of one half
+    // runs (on a high-priority stream) under the streaming Gram / update of
+    // the other.  Order per p-step s, halves A = [0, T/2), B = [T/2, T):
+    //   sA: gram(A) -> [inner(A) on sI] -> update(A)
+    //   sB: (after gram(A)) gram(B) -> [inner(B) on sI] -> update(B)
+    //   next p-step starts after both updates (block-columns move between
+    //   halves from one p-step to the next).
+    static cudaStream_t sA = nullptr, sB = nullptr, sI = nullptr;
+    static cudaEvent_t ev[8];
+    if (!sA) {
+      int lo, hi;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      cudaStreamCreateWithPriority(&sA, cudaStreamNonBlocking, lo);
+      cudaStreamCreateWithPriority(&sB, cudaStreamNonBlocking, lo);
+      cudaStreamCreateWithPriority(&sI, cudaStreamNonBlocking, hi);
+      for (auto &e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    }
+    enum { kStart, kGA, kIA, kGB, kIB, kUB, kJoin };
+    cudaEventRecord(ev[kStart], st);
+    cudaStreamWaitEvent(sA, ev[kStart], 0);
+    cudaStreamWaitEvent(sB, ev[kStart], 0);
+    cudaStreamWaitEvent(sI, ev[kStart], 0);
+    const int tA = ntask / 2, tB = ntask - tA;
+    const size_t ww = (size_t)w * w;
+    auto half = [&](const int32_t *pairs_s, int t0, int nt, cudaStream_t sx, cudaEvent_t eg,
+                    cudaEvent_t ei, int s) {
+      const int32_t *pr = pairs_s + 2 * t0;
+      prof_mark(sx, 0, false);
+      launch_gram_tma(G, ldg, m, pr, nt, w, Hbuf + t0 * ww, sx);
+      prof_mark(sx, 0, true);
+      cudaEventRecord(eg, sx);
+      cudaStreamWaitEvent(sI, eg, 0);
+      prof_mark(sI, 1, false);
+      launch_inner3(Hbuf + t0 * ww, Vbuf + t0 * ww, trot + t0, pr, nt, w, n_plus, inner,
+                    inner_limit, tol_c, counters, s, sI, t0);
+      prof_mark(sI, 1, true);
+      cudaEventRecord(ei, sI);
+      cudaStreamWaitEvent(sx, ei, 0);
+      prof_mark(sx, 2, false);
+      launch_update_dmma(G, ldg, m, V, ldv, nv, pr, nt, w, Vbuf + t0 * ww, trot + t0, sx);
+      prof_mark(sx, 2, true);
+      g_launches += 3;
+    };
+    for (int s = first_step; s < first_step + nsteps; s++) {
+      const int32_t *pairs = outer + (int64_t)s * ntask * 2;
+      half(pairs, 0, tA, sA, ev[kGA], ev[kIA], s);
+      cudaStreamWaitEvent(sB, ev[kGA], 0);  // stagger B behind A's Gram
+      half(pairs, tA, tB, sB, ev[kGB], ev[kIB], s);
+      cudaEventRecord(ev[kUB], sB);
+      cudaStreamWaitEvent(sA, ev[kUB], 0);  // join: the p-step is complete on sA
+      cudaEventRecord(ev[kJoin], sA);
+      cudaStreamWaitEvent(sB, ev[kJoin], 0);
+      cudaStreamWaitEvent(sI, ev[kJoin], 0);
+    }
+    cudaEventRecord(ev[kJoin], sA);
+    cudaStreamWaitEvent(st, ev[kJoin], 0);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : -(int)e;
+  }
   for (int s = first_step; s < first_step + nsteps; s++) {
     const int32_t *pairs = outer + (int64_t)s * ntask * 2;
     prof_mark(st, 0, false);

@@ -87,6 +87,8 @@ def test_block_jacobi_bitwise_vs_reference(name, solves_golden):
     (1024, 32, "rrow", "full-block", 1024),
     (768, 16, "mm", "block-oriented", 300),
     (512, 64, "rrow", "full-block", 512),
+    (1024, 16, "rrow", "full-block", 1024),   # 64 tasks: two-stream split path
+    (1024, 16, "bl", "block-oriented", 1024),
 ])
 def test_block_jacobi_bitwise_vs_oracle(n, w, kind, variant, nplus, oracle):
     rng = np.random.default_rng(n + w)
