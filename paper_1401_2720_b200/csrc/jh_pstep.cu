@@ -746,66 +746,77 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
   static const bool force_simple = getenv("JHSVD_FORCE_SIMPLE") != nullptr;
   const bool use_tma_gram = !force_simple && gram_tma_ok(w, m, ldg);
   const bool use_dmma_update = !force_simple && update_dmma_ok(w);
-  static const char *env_streams = getenv("JHSVD_STREAMS");
-  const bool split = use_tma_gram && use_dmma_update && inner3_ok(w) && ntask >= 64 &&
-                     !(env_streams && env_streams[0] == '0');
-  if (split) {
-    // Two half-p-steps in flight: the latency-bound inner Jacobi of one half
-    // runs (on a high-priority stream) under the streaming Gram / update of
-    // the other.  Order per p-step s, halves A = [0, T/2), B = [T/2, T):
-    //   sA: gram(A) -> [inner(A) on sI] -> update(A)
-    //   sB: (after gram(A)) gram(B) -> [inner(B) on sI] -> update(B)
-    //   next p-step starts after both updates (block-columns move between
-    //   halves from one p-step to the next).
-    static cudaStream_t sA = nullptr, sB = nullptr, sI = nullptr;
-    static cudaEvent_t ev[8];
-    if (!sA) {
+  // K-way staggered pipeline of a p-step (JHSVD_STREAMS = K, 0/1 disables)
+  static const int env_k = [] {
+    const char *e = getenv("JHSVD_STREAMS");
+    return e ? atoi(e) : 4;
+  }();
+  const int K = (use_tma_gram && use_dmma_update && inner3_ok(w)) ? env_k : 0;
+  if (K >= 2 && ntask >= 16 * K) {
+    // The tasks of a p-step are split into K parts.  Part k's Gram follows
+    // part k-1's on one stream (so the Grams stream back to back at full
+    // bandwidth), its latency-bound inner Jacobi runs on its own
+    // high-priority stream as soon as its Gram is done, and its update
+    // follows its inner Jacobi.  The inner phases of all parts but the first
+    // thus run under other parts' streaming kernels.  The next p-step starts
+    // after all updates (block-columns move between parts across p-steps).
+    constexpr int KMAX = 8;
+    static cudaStream_t sP[KMAX], sI[KMAX];
+    static cudaEvent_t eG[KMAX], eI[KMAX], eU[KMAX], eStart, eJoin;
+    static bool init = false;
+    if (!init) {
       int lo, hi;
       cudaDeviceGetStreamPriorityRange(&lo, &hi);
-      cudaStreamCreateWithPriority(&sA, cudaStreamNonBlocking, lo);
-      cudaStreamCreateWithPriority(&sB, cudaStreamNonBlocking, lo);
-      cudaStreamCreateWithPriority(&sI, cudaStreamNonBlocking, hi);
-      for (auto &e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      for (int k = 0; k < KMAX; k++) {
+        cudaStreamCreateWithPriority(&sP[k], cudaStreamNonBlocking, lo);
+        cudaStreamCreateWithPriority(&sI[k], cudaStreamNonBlocking, hi);
+        cudaEventCreateWithFlags(&eG[k], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&eI[k], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&eU[k], cudaEventDisableTiming);
+      }
+      cudaEventCreateWithFlags(&eStart, cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&eJoin, cudaEventDisableTiming);
+      init = true;
     }
-    enum { kStart, kGA, kIA, kGB, kIB, kUB, kJoin };
-    cudaEventRecord(ev[kStart], st);
-    cudaStreamWaitEvent(sA, ev[kStart], 0);
-    cudaStreamWaitEvent(sB, ev[kStart], 0);
-    cudaStreamWaitEvent(sI, ev[kStart], 0);
-    const int tA = ntask / 2, tB = ntask - tA;
+    const int KK = K > KMAX ? KMAX : K;
     const size_t ww = (size_t)w * w;
-    auto half = [&](const int32_t *pairs_s, int t0, int nt, cudaStream_t sx, cudaEvent_t eg,
-                    cudaEvent_t ei, int s) {
-      const int32_t *pr = pairs_s + 2 * t0;
-      prof_mark(sx, 0, false);
-      launch_gram_tma(G, ldg, m, pr, nt, w, Hbuf + t0 * ww, sx);
-      prof_mark(sx, 0, true);
-      cudaEventRecord(eg, sx);
-      cudaStreamWaitEvent(sI, eg, 0);
-      prof_mark(sI, 1, false);
-      launch_inner3(Hbuf + t0 * ww, Vbuf + t0 * ww, trot + t0, pr, nt, w, n_plus, inner,
-                    inner_limit, tol_c, counters, s, sI, t0);
-      prof_mark(sI, 1, true);
-      cudaEventRecord(ei, sI);
-      cudaStreamWaitEvent(sx, ei, 0);
-      prof_mark(sx, 2, false);
-      launch_update_dmma(G, ldg, m, V, ldv, nv, pr, nt, w, Vbuf + t0 * ww, trot + t0, sx);
-      prof_mark(sx, 2, true);
-      g_launches += 3;
-    };
+    cudaEventRecord(eStart, st);
+    for (int k = 0; k < KK; k++) {
+      cudaStreamWaitEvent(sP[k], eStart, 0);
+      cudaStreamWaitEvent(sI[k], eStart, 0);
+    }
     for (int s = first_step; s < first_step + nsteps; s++) {
       const int32_t *pairs = outer + (int64_t)s * ntask * 2;
-      half(pairs, 0, tA, sA, ev[kGA], ev[kIA], s);
-      cudaStreamWaitEvent(sB, ev[kGA], 0);  // stagger B behind A's Gram
-      half(pairs, tA, tB, sB, ev[kGB], ev[kIB], s);
-      cudaEventRecord(ev[kUB], sB);
-      cudaStreamWaitEvent(sA, ev[kUB], 0);  // join: the p-step is complete on sA
-      cudaEventRecord(ev[kJoin], sA);
-      cudaStreamWaitEvent(sB, ev[kJoin], 0);
-      cudaStreamWaitEvent(sI, ev[kJoin], 0);
+      for (int k = 0; k < KK; k++) {
+        const int t0 = (int)((int64_t)ntask * k / KK);
+        const int nt = (int)((int64_t)ntask * (k + 1) / KK) - t0;
+        const int32_t *pr = pairs + 2 * t0;
+        cudaStream_t sx = sP[k], si = sI[k];
+        if (k > 0) cudaStreamWaitEvent(sx, eG[k - 1], 0);  // Grams back to back
+        prof_mark(sx, 0, false);
+        launch_gram_tma(G, ldg, m, pr, nt, w, Hbuf + t0 * ww, sx);
+        prof_mark(sx, 0, true);
+        cudaEventRecord(eG[k], sx);
+        cudaStreamWaitEvent(si, eG[k], 0);
+        prof_mark(si, 1, false);
+        launch_inner3(Hbuf + t0 * ww, Vbuf + t0 * ww, trot + t0, pr, nt, w, n_plus, inner,
+                      inner_limit, tol_c, counters, s, si, t0);
+        prof_mark(si, 1, true);
+        cudaEventRecord(eI[k], si);
+        cudaStreamWaitEvent(sx, eI[k], 0);
+        prof_mark(sx, 2, false);
+        launch_update_dmma(G, ldg, m, V, ldv, nv, pr, nt, w, Vbuf + t0 * ww, trot + t0, sx);
+        prof_mark(sx, 2, true);
+        cudaEventRecord(eU[k], sx);
+        g_launches += 3;
+      }
+      // join: every part of the next p-step waits for all updates
+      for (int k = 1; k < KK; k++) cudaStreamWaitEvent(sP[0], eU[k], 0);
+      cudaEventRecord(eJoin, sP[0]);
+      for (int k = 1; k < KK; k++) cudaStreamWaitEvent(sP[k], eJoin, 0);
     }
-    cudaEventRecord(ev[kJoin], sA);
-    cudaStreamWaitEvent(st, ev[kJoin], 0);
+    cudaEventRecord(eJoin, sP[0]);
+    cudaStreamWaitEvent(st, eJoin, 0);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : -(int)e;
   }
