@@ -111,6 +111,11 @@ int jh_probe_dmma(const double *A, const double *B, const double *C, double *Dm,
  * runs 8 independent chains for `iters` iterations. */
 int jh_probe_rate(int kind, int ctas, int threads, int iters, double *out, void *stream);
 
+/* Diagnostic: inner-Jacobi phase timing (cycles of warp 0 in dots, rotation,
+ * barrier, R apply, barrier; inner p-steps; inner sweeps; tasks).  on = 1
+ * enables, 0 disables; out (host uint64[8]) receives and resets them. */
+int jh_inner_profile(int on, unsigned long long *out);
+
 /* Diagnostic: dependent-chain latencies (cycles/op) of DFMA, DMUL, division,
  * sqrt, the rotation formula and a shared-memory load; out[6]. */
 int jh_probe_latency(double *out, void *stream);

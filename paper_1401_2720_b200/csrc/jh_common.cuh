@@ -71,6 +71,38 @@ __device__ __forceinline__ bool rotation_core(double hpp, double hqq, double hpq
   return true;
 }
 
+// Branch-light form of rotation_core with identical results: every special
+// case (hyperbolic 5/4 substitution and domain check, the sqrt(eps) and
+// sqrt(2/eps) guards) becomes a select, so the two square roots and three
+// divisions issue without divergence and the critical path is
+// div -> sqrt -> sqrt -> div.  Values computed on a discarded branch (NaN /
+// inf from sqrt of a negative or an overflowing square) never reach a result.
+__device__ __forceinline__ bool rotation_core_sel(double hpp, double hqq, double hpq, double t,
+                                                  double &cs, double &tn) {
+  const double h = hqq - t * hpp;
+  double ct2 = t * (h / (2.0 * hpq));
+  bool ok = true;
+  if (t < 0.0) {
+    const double aa = fabs(ct2);
+    ok = !(aa < 1.0);
+    ct2 = (aa == 1.0) ? (ct2 > 0.0 ? 1.25 : -1.25) : ct2;
+  }
+  const double a = fabs(ct2);
+  const double sgn = ct2 >= 0.0 ? 1.0 : -1.0;
+  const double r = sqrt(fma(ct2, ct2, t));
+  const bool huge = a >= kCt2Huge;
+  double ct = (t > 0.0 && a < kCt2Tiny) ? a + 1.0 : a + r;
+  ct = huge ? 2.0 * a : ct;
+  tn = sgn / ct;
+  const double c2 = ct / sqrt(fma(ct, ct, t));
+  cs = huge ? 1.0 : c2;
+  if (!ok) {
+    cs = 0.0;
+    tn = 0.0;
+  }
+  return ok;
+}
+
 __host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 

@@ -17,6 +17,12 @@
 
 namespace jh {
 
+// optional phase timing of the inner Jacobi (jh_inner_profile): cycles spent
+// by warp 0 in [dots, rotation, barrier 1, R apply, barrier 2], the number of
+// inner p-steps, inner sweeps and tasks
+__device__ int g_inner_prof_on = 0;
+__device__ unsigned long long g_inner_prof[8];
+
 template <int W>
 struct InnerCfg {
   static constexpr int HALF = W / 2;
@@ -59,6 +65,49 @@ __device__ __forceinline__ void rot_apply(double *M, int ld, int p, int q, int i
     *mp = np;
     *mq = nq;
   }
+}
+
+// Rotate rows i of the pairs g0, g0 + STRIDE, ... (< HALF) of one inner
+// p-step.  All parameters and operands are loaded first (independent
+// shared-memory loads in flight together), then the rotated pairs are
+// written; a pair that was not rotated is left untouched bit for bit.
+template <int HALF, int STRIDE>
+__device__ __forceinline__ void apply_rows(double *M, int ld, const int8_t *st,
+                                           const StepParams *prm, int g0, int i) {
+  constexpr int NP = (HALF + STRIDE - 1) / STRIDE;
+  int act[NP], p[NP], q[NP];
+  double cs[NP], tn[NP], gp[NP], gq[NP];
+#pragma unroll
+  for (int k = 0; k < NP; k++) {
+    const int pi = g0 + k * STRIDE;
+    act[k] = 0;
+    if (pi < HALF) {
+      act[k] = prm[pi].act;
+      cs[k] = prm[pi].cs;
+      tn[k] = prm[pi].tn;
+      p[k] = st[2 * pi];
+      q[k] = st[2 * pi + 1];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NP; k++)
+    if (act[k]) {
+      gp[k] = M[p[k] * ld + i];
+      gq[k] = M[q[k] * ld + i];
+    }
+#pragma unroll
+  for (int k = 0; k < NP; k++)
+    if (act[k]) {
+      const double s = (act[k] & 4) ? tn[k] : -tn[k];
+      double np = fma(s, gq[k], gp[k]), nq = fma(tn[k], gp[k], gq[k]);
+      if (cs[k] != 1.0) {
+        np = np * cs[k];
+        nq = nq * cs[k];
+      }
+      const bool sw = (act[k] & 3) == 2;
+      M[p[k] * ld + i] = sw ? nq : np;
+      M[q[k] * ld + i] = sw ? np : nq;
+    }
 }
 
 template <int W>
@@ -137,10 +186,14 @@ k_factor_inner3(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
   const int ri = tid % W;         // row handled in the R / V applies
   const int rg = tid / W;         // pair group
   constexpr int RGS = NTH / W;    // pair groups in the R apply
+  const bool prof = g_inner_prof_on != 0;
+  unsigned long long pt[5] = {0, 0, 0, 0, 0};
+  long long c0 = 0, c1 = 0;
   for (int sw = 0; sw < inner_limit && !status; sw++) {
     for (int si = 0; si < NSTEP; si++, gstep++) {
       const int8_t *st = S.steps + si * W;
       StepParams *cur = S.prm[gstep & 1];
+      if (prof && tid == 0) c0 = clock64();
       if (warp == 0) {
         int fail = 0, fb = 0;
         if (lane < HALF) {
@@ -158,9 +211,14 @@ k_factor_inner3(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
           // the rotation is formed speculatively, in parallel with the
           // orthogonality test (it has no side effects; a pair that passes
           // the test discards it, exactly like the reference never forms it)
+          if (prof && lane == 0) {
+            c1 = clock64() + (long long)(hpp * 0.0);
+            pt[0] += c1 - c0;
+            c0 = c1;
+          }
           const bool hyp = S.sg[p] > 0 && S.sg[q] < 0;
           double cs, tn;
-          const bool rot_ok = rotation_core(hpp, hqq, hpq, hyp ? -1.0 : 1.0, cs, tn);
+          const bool rot_ok = rotation_core_sel(hpp, hqq, hpq, hyp ? -1.0 : 1.0, cs, tn);
           if (hpp == 0.0) {
             fail = kZeroColumn;
             fb = p + 1;
@@ -185,6 +243,11 @@ k_factor_inner3(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
             }
           }
           cur[lane] = pr;
+          if (prof && lane == 0) {
+            c1 = clock64();
+            pt[1] += c1 - c0;
+            c0 = c1;
+          }
         }
         const unsigned fm = __ballot_sync(0xffffffffu, fail != 0);
         if (fm) {
@@ -203,20 +266,28 @@ k_factor_inner3(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
         const StepParams *prev = S.prm[(gstep - 1) & 1];
         const int vt = tid - 32, vrow = vt % W, vg = vt / W;
         constexpr int VGS = (NTH - 32) / W;
-        if (vt < VGS * W)
-          for (int pi = vg; pi < HALF; pi += VGS)
-            if (prev[pi].act) rot_apply(S.V, LD, pst[2 * pi], pst[2 * pi + 1], vrow, prev[pi]);
+        if (vt < VGS * W) apply_rows<HALF, VGS>(S.V, LD, pst, prev, vg, vrow);
       }
       __syncthreads();
+      if (prof && tid == 0) {
+        c1 = clock64();
+        pt[2] += c1 - c0;
+        c0 = c1;
+      }
       if (S.stop) {
         status = S.fail_status;
         bad = S.fail_bad;
         break;
       }
       // R update of this inner p-step (all threads)
-      for (int pi = rg; pi < HALF; pi += RGS)
-        if (cur[pi].act) rot_apply(S.R, LD, st[2 * pi], st[2 * pi + 1], ri, cur[pi]);
+      apply_rows<HALF, RGS>(S.R, LD, st, cur, rg, ri);
+      if (prof && tid == 0) {
+        c1 = clock64();
+        pt[3] += c1 - c0;
+        c0 = c1;
+      }
       __syncthreads();
+      if (prof && tid == 0) pt[4] += clock64() - c0;
     }
     if (status) break;
     // sweep end: totals of applied / proper rotations
@@ -249,14 +320,19 @@ k_factor_inner3(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
     const int last = (gstep - 1) % NSTEP;
     const int8_t *pst = S.steps + last * W;
     const StepParams *prev = S.prm[(gstep - 1) & 1];
-    for (int pi = rg; pi < HALF; pi += RGS)
-      if (prev[pi].act) rot_apply(S.V, LD, pst[2 * pi], pst[2 * pi + 1], ri, prev[pi]);
+    apply_rows<HALF, RGS>(S.V, LD, pst, prev, rg, ri);
   }
   __syncthreads();
   double *Vg = Vbuf + (size_t)task * W * W;
   for (int e = tid; e < W * W; e += NTH) {
     const int j = e / W, i = e - j * W;
     Vg[e] = S.V[j * LD + i];
+  }
+  if (prof && tid == 0) {
+    for (int k = 0; k < 5; k++) atomicAdd(&g_inner_prof[k], pt[k]);
+    atomicAdd(&g_inner_prof[5], (unsigned long long)gstep);
+    atomicAdd(&g_inner_prof[6], (unsigned long long)sweeps);
+    atomicAdd(&g_inner_prof[7], 1ull);
   }
   if (tid == 0) {
     task_rot[task] = tot_rot;
@@ -301,3 +377,18 @@ void launch_inner3(const double *Hbuf, double *Vbuf, int64_t *trot, const int32_
 }
 
 }  // namespace jh
+
+// Enable (1) / disable (0) inner-Jacobi phase timing; when out != NULL,
+// copies the 8 accumulated counters (see g_inner_prof) to host memory and
+// resets them.
+extern "C" int jh_inner_profile(int on, unsigned long long *out) {
+  cudaDeviceSynchronize();
+  if (out) {
+    cudaMemcpyFromSymbol(out, jh::g_inner_prof, sizeof(unsigned long long) * 8);
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(jh::g_inner_prof, z, sizeof(z));
+  }
+  cudaMemcpyToSymbol(jh::g_inner_prof_on, &on, sizeof(int));
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : -(int)e;
+}

@@ -749,7 +749,7 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
   // K-way staggered pipeline of a p-step (JHSVD_STREAMS = K, 0/1 disables)
   static const int env_k = [] {
     const char *e = getenv("JHSVD_STREAMS");
-    return e ? atoi(e) : 4;
+    return e ? atoi(e) : 0;
   }();
   const int K = (use_tma_gram && use_dmma_update && inner3_ok(w)) ? env_k : 0;
   if (K >= 2 && ntask >= 16 * K) {

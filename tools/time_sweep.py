@@ -65,5 +65,37 @@ def main():
             print(f"   {names[k]:13s} {pms[k]:9.2f} ms total, {per * 1e3:9.1f} us/launch{extra}")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--inner" not in sys.argv:
     main()
+
+
+def inner_profile(n=4096, w=32, steps=8):
+    """Phase timing of the inner Jacobi (cycles per inner p-step)."""
+    import ctypes
+
+    from paper_1401_2720_b200 import _lib
+
+    lib = _lib.load_library()
+    cfg = SolverConfig(block_width=w)
+    eng = SweepEngine(n, n, n, cfg, make_strategy("rrow", n // (w // 2)), make_strategy("rrow", w), n)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    G = torch.randn(n, n, dtype=torch.float64, device="cuda", generator=g)
+    V = torch.eye(n, dtype=torch.float64, device="cuda")
+    out = (ctypes.c_ulonglong * 8)()
+    lib.jh_inner_profile(1, None)
+    eng.sweep(G, V, 0, steps)
+    lib.jh_inner_profile(0, out)
+    v = list(out)
+    nst = max(v[5], 1)
+    names = ["dots", "rotation", "barrier1", "apply_R", "barrier2"]
+    print(f"inner profile n={n} w={w}: {v[7]} tasks, {v[6] / max(v[7], 1):.2f} inner sweeps/task, "
+          f"{v[5] / max(v[7], 1):.1f} inner p-steps/task")
+    tot = sum(v[:5]) / nst
+    for k in range(5):
+        print(f"   {names[k]:9s} {v[k] / nst:8.1f} cycles/step")
+    print(f"   total     {tot:8.1f} cycles/step")
+
+
+if __name__ == "__main__" and "--inner" in sys.argv:
+    args = [a for a in sys.argv[1:] if a != "--inner"]
+    inner_profile(*(int(a) for a in args))
