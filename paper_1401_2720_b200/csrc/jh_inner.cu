@@ -392,3 +392,327 @@ extern "C" int jh_inner_profile(int on, unsigned long long *out) {
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : -(int)e;
 }
+
+namespace jh {
+
+// ===========================================================================
+// K2 v4 (W = 16, 32): one warp owns R in registers.
+//
+// Lane group g (LPP = 32 / (W/2) lanes) holds the two columns of pair g of
+// the current inner p-step, RPL = W / LPP rows per lane.  Dots: the three
+// in-order fma chains run through the group's lanes in row order (partial
+// chain in lane k, handed to lane k+1 by a shuffle), so each value is the
+// reference's chain; the last lane broadcasts the sums and every lane of the
+// group forms the same rotation parameters.  Each lane rotates its rows in
+// registers, then the columns are redistributed for the next p-step through
+// shared memory with __syncwarp only.  Warp 1 applies the rotations to V
+// from a ring of per-step parameters, lagging behind; warps 0 and 1 only
+// synchronise through shared counters.  No CTA barrier on the critical path.
+
+constexpr int kRing = 8;
+
+template <int W>
+struct Inner4Smem {
+  double H[W * W];
+  double R[W * (W + 2)];     // column exchange buffer, stride W + 2
+  double V[W * (W + 1)];
+  StepParams prm[kRing][W / 2];
+  int8_t steps[(W - 1) * W];
+  int8_t sg[W];
+  int chol, status, bad;
+  volatile int produced;      // inner p-steps published by warp 0
+  volatile int consumed;      // inner p-steps applied to V by warp 1
+  volatile int finished;      // warp 0 done: total steps in `produced`
+};
+
+template <int W>
+__global__ void __launch_bounds__(64)
+k_factor_inner4(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
+                int64_t *__restrict__ task_rot, const int32_t *__restrict__ pairs,
+                int64_t n_plus, const int32_t *__restrict__ inner, int inner_limit,
+                double tol_c, unsigned long long *counters, int pstep, int task_base) {
+  constexpr int HALF = W / 2, NSTEP = W - 1, BW = W / 2;
+  constexpr int LPP = 32 / HALF;     // lanes per pair
+  constexpr int RPL = W / LPP;       // rows per lane
+  constexpr int LDR = W + 2, LDV = W + 1;
+  constexpr int NTH = 64;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  Inner4Smem<W> &S = *reinterpret_cast<Inner4Smem<W> *>(smraw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int task = blockIdx.x;
+  const int p0 = pairs[2 * task], q0 = pairs[2 * task + 1];
+
+  const double *Hg = Hbuf + (size_t)task * W * W;
+  for (int i = tid; i < W * W; i += NTH) S.H[i] = Hg[i];
+  for (int i = tid; i < W * LDV; i += NTH) {
+    const int col = i / LDV, row = i - col * LDV;
+    S.V[i] = (row == col) ? 1.0 : 0.0;
+  }
+  for (int i = tid; i < NSTEP * W; i += NTH) S.steps[i] = (int8_t)inner[i];
+  for (int j = tid; j < W; j += NTH) {
+    const int64_t gcol = (j < BW ? (int64_t)p0 * BW + j : (int64_t)q0 * BW + (j - BW)) + 1;
+    S.sg[j] = gcol <= n_plus ? 1 : -1;
+  }
+  if (tid == 0) {
+    S.chol = 0;
+    S.status = 0;
+    S.produced = 0;
+    S.consumed = 0;
+    S.finished = 0;
+  }
+  __syncthreads();
+  // forward-looking Cholesky (reference element order)
+  {
+    const int x = tid % W, jg = tid / W;
+    constexpr int JS = NTH / W;
+    for (int k = 0; k < W; k++) {
+      if (tid == 0) {
+        const double d = S.H[k * W + k];
+        if (!(d > 0.0) || !isfinite(d))
+          S.chol = k + 1;
+        else
+          S.H[k * W + k] = sqrt(d);
+      }
+      __syncthreads();
+      if (S.chol) break;
+      const double l = S.H[k * W + k];
+      if (jg == 0 && x > k) S.H[k * W + x] = S.H[k * W + x] / l;
+      __syncthreads();
+      for (int j = k + 1 + jg; j < W; j += JS)
+        if (x >= j) S.H[j * W + x] = fma(-S.H[k * W + x], S.H[k * W + j], S.H[j * W + x]);
+      __syncthreads();
+    }
+  }
+  if (S.chol) {
+    if (tid == 0) {
+      task_rot[task] = 0;
+      atomicMin(&counters[2], err_key(pstep, task_base + task, kCholesky, S.chol));
+    }
+    return;
+  }
+  for (int e = tid; e < W * W; e += NTH) {
+    const int j = e / W, i = e - j * W;
+    S.R[j * LDR + i] = (i <= j) ? S.H[i * W + j] : 0.0;
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ---------------- R owner ----------------
+    const int gi = lane / LPP, k = lane % LPP;  // pair, position in the group
+    const int r0 = k * RPL;
+    int p = S.steps[2 * gi], q = S.steps[2 * gi + 1];
+    double cp[RPL], cq[RPL];
+#pragma unroll
+    for (int r = 0; r < RPL; r++) {
+      cp[r] = S.R[p * LDR + r0 + r];
+      cq[r] = S.R[q * LDR + r0 + r];
+    }
+    int64_t tot_rot = 0, tot_proper = 0;
+    int gstep = 0, status = 0, bad = -1;
+    for (int sw = 0; sw < inner_limit && !status; sw++) {
+      int a_r = 0, b_r = 0;
+      for (int si = 0; si < NSTEP; si++, gstep++) {
+        // dots: chains through the group's lanes in row order
+        double hpp = 0.0, hqq = 0.0, hpq = 0.0;
+#pragma unroll
+        for (int j = 0; j < LPP; j++) {
+          if (k == j) {
+#pragma unroll
+            for (int r = 0; r < RPL; r++) {
+              hpp = fma(cp[r], cp[r], hpp);
+              hqq = fma(cq[r], cq[r], hqq);
+              hpq = fma(cp[r], cq[r], hpq);
+            }
+          }
+          if (j + 1 < LPP) {
+            // hand the partial chains to the next lane of the group
+            const int src = gi * LPP + j;
+            const double a = __shfl_sync(0xffffffffu, hpp, src);
+            const double b = __shfl_sync(0xffffffffu, hqq, src);
+            const double c = __shfl_sync(0xffffffffu, hpq, src);
+            if (k == j + 1) {
+              hpp = a;
+              hqq = b;
+              hpq = c;
+            }
+          }
+        }
+        {
+          const int src = gi * LPP + LPP - 1;
+          hpp = __shfl_sync(0xffffffffu, hpp, src);
+          hqq = __shfl_sync(0xffffffffu, hqq, src);
+          hpq = __shfl_sync(0xffffffffu, hpq, src);
+        }
+        const bool hyp = S.sg[p] > 0 && S.sg[q] < 0;
+        double cs, tn;
+        const bool rot_ok = rotation_core_sel(hpp, hqq, hpq, hyp ? -1.0 : 1.0, cs, tn);
+        int act = 0, fail = 0, fb = 0;
+        if (hpp == 0.0) {
+          fail = kZeroColumn;
+          fb = p + 1;
+        } else if (hqq == 0.0) {
+          fail = kZeroColumn;
+          fb = q + 1;
+        } else if (!(fabs(hpq) < tol_c * sqrt(hpp) * sqrt(hqq))) {
+          if (!rot_ok) {
+            fail = kHypDomain;
+            fb = p + 1;
+          } else {
+            act = hyp ? 5 : 1;
+            if (!hyp) {
+              const double h1 = fma(-tn, hpq, hpp);
+              const double h2 = fma(tn, hpq, hqq);
+              if ((S.sg[p] > 0 && h1 < h2) || (S.sg[p] < 0 && h1 > h2)) act = 2;
+            }
+          }
+        }
+        const unsigned fm = __ballot_sync(0xffffffffu, fail != 0);
+        if (fm) {
+          const int first = __ffs(fm) - 1;  // lowest pair fails first in reference order
+          status = __shfl_sync(0xffffffffu, fail, first);
+          bad = __shfl_sync(0xffffffffu, fb, first);
+          break;
+        }
+        if (act && k == 0) {
+          a_r++;
+          if (cs != 1.0) b_r++;
+        }
+        // publish for the V warp (ring slot free once V consumed step gstep - kRing)
+        if (k == 0) {
+          while (gstep - S.consumed >= kRing) {
+          }
+          StepParams pr;
+          pr.cs = cs;
+          pr.tn = tn;
+          pr.act = act;
+          S.prm[gstep % kRing][gi] = pr;
+        }
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence_block();
+          S.produced = gstep + 1;
+        }
+        // rotate my rows in registers
+        if (act) {
+          const double s = (act & 4) ? tn : -tn;
+          const bool scale = cs != 1.0, swp = (act & 3) == 2;
+#pragma unroll
+          for (int r = 0; r < RPL; r++) {
+            double np = fma(s, cq[r], cp[r]), nq = fma(tn, cp[r], cq[r]);
+            if (scale) {
+              np = np * cs;
+              nq = nq * cs;
+            }
+            cp[r] = swp ? nq : np;
+            cq[r] = swp ? np : nq;
+          }
+        }
+        // redistribute columns for the next inner p-step
+        const int nsi = (si + 1 == NSTEP) ? 0 : si + 1;
+#pragma unroll
+        for (int r = 0; r < RPL; r++) {
+          S.R[p * LDR + r0 + r] = cp[r];
+          S.R[q * LDR + r0 + r] = cq[r];
+        }
+        __syncwarp();  // all columns of this step written
+        p = S.steps[nsi * W + 2 * gi];
+        q = S.steps[nsi * W + 2 * gi + 1];
+#pragma unroll
+        for (int r = 0; r < RPL; r++) {
+          cp[r] = S.R[p * LDR + r0 + r];
+          cq[r] = S.R[q * LDR + r0 + r];
+        }
+        __syncwarp();
+      }
+      if (status) break;
+      const int ta = __reduce_add_sync(0xffffffffu, a_r);
+      const int tb = __reduce_add_sync(0xffffffffu, b_r);
+      tot_rot += ta;
+      tot_proper += tb;
+      if (ta == 0) break;
+    }
+    if (lane == 0) {
+      S.status = status;
+      S.bad = bad;
+      __threadfence_block();
+      S.finished = 1;
+    }
+    if (lane == 0 && !status) {
+      task_rot[task] = tot_rot;
+      atomicAdd(&counters[0], (unsigned long long)tot_rot);
+      atomicAdd(&counters[1], (unsigned long long)tot_proper);
+      if (tot_rot) atomicAdd(&counters[3], 1ull);
+    }
+  } else {
+    // ---------------- V applier (warp 1): lane = row ----------------
+    int done = 0;
+    for (;;) {
+      int avail = S.produced;
+      if (avail == done) {
+        if (S.finished) {
+          avail = S.produced;
+          if (avail == done) break;
+        } else {
+          continue;
+        }
+      }
+      __threadfence_block();
+      for (; done < avail; done++) {
+        const int si = done % NSTEP;
+        const int8_t *st = S.steps + si * W;
+        const StepParams *pr = S.prm[done % kRing];
+        if (lane < W) {
+#pragma unroll
+          for (int g0 = 0; g0 < 4; g0++) apply_rows<HALF, 4>(S.V, LDV, st, pr, g0, lane);
+        }
+        __syncwarp();
+        if (lane == 0) S.consumed = done + 1;
+      }
+    }
+  }
+  __syncthreads();
+  if (S.status) {
+    if (tid == 0) {
+      task_rot[task] = 0;
+      atomicMin(&counters[2], err_key(pstep, task_base + task, S.status, S.bad));
+    }
+    return;
+  }
+  double *Vg = Vbuf + (size_t)task * W * W;
+  for (int e = tid; e < W * W; e += NTH) {
+    const int j = e / W, i = e - j * W;
+    Vg[e] = S.V[j * LDV + i];
+  }
+}
+
+bool inner4_ok(int w) { return w == 16 || w == 32; }
+
+template <int W>
+static void launch_inner4_t(const double *Hbuf, double *Vbuf, int64_t *trot, const int32_t *pairs,
+                            int ntask, int64_t n_plus, const int32_t *inner, int inner_limit,
+                            double tol_c, unsigned long long *counters, int pstep,
+                            cudaStream_t st, int task_base) {
+  const size_t smem = sizeof(Inner4Smem<W>);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_factor_inner4<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr = true;
+  }
+  k_factor_inner4<W><<<ntask, 64, smem, st>>>(Hbuf, Vbuf, trot, pairs, n_plus, inner, inner_limit,
+                                              tol_c, counters, pstep, task_base);
+}
+
+void launch_inner4(const double *Hbuf, double *Vbuf, int64_t *trot, const int32_t *pairs,
+                   int ntask, int w, int64_t n_plus, const int32_t *inner, int inner_limit,
+                   double tol_c, unsigned long long *counters, int pstep, cudaStream_t st,
+                   int task_base) {
+  if (w == 16)
+    launch_inner4_t<16>(Hbuf, Vbuf, trot, pairs, ntask, n_plus, inner, inner_limit, tol_c,
+                        counters, pstep, st, task_base);
+  else
+    launch_inner4_t<32>(Hbuf, Vbuf, trot, pairs, ntask, n_plus, inner, inner_limit, tol_c,
+                        counters, pstep, st, task_base);
+}
+
+}  // namespace jh

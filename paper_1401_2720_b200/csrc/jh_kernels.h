@@ -24,4 +24,11 @@ void launch_inner3(const double *Hbuf, double *Vbuf, int64_t *trot, const int32_
                    double tol_c, unsigned long long *counters, int pstep, cudaStream_t st,
                    int task_base = 0);
 
+// register-resident inner Jacobi, w in {16, 32} (jh_inner.cu)
+bool inner4_ok(int w);
+void launch_inner4(const double *Hbuf, double *Vbuf, int64_t *trot, const int32_t *pairs,
+                   int ntask, int w, int64_t n_plus, const int32_t *inner, int inner_limit,
+                   double tol_c, unsigned long long *counters, int pstep, cudaStream_t st,
+                   int task_base = 0);
+
 }  // namespace jh

@@ -746,6 +746,8 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
   static const bool force_simple = getenv("JHSVD_FORCE_SIMPLE") != nullptr;
   const bool use_tma_gram = !force_simple && gram_tma_ok(w, m, ldg);
   const bool use_dmma_update = !force_simple && update_dmma_ok(w);
+  static const char *env_inner = getenv("JHSVD_INNER");  // "3" selects the v3 kernel
+  const bool use_inner4 = !force_simple && inner4_ok(w) && !(env_inner && env_inner[0] == '3');
   // K-way staggered pipeline of a p-step (JHSVD_STREAMS = K, 0/1 disables)
   static const int env_k = [] {
     const char *e = getenv("JHSVD_STREAMS");
@@ -832,6 +834,9 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
     if (force_simple)
       k_factor_inner<<<ntask, thr_inner, smem_inner, st>>>(Hbuf, Vbuf, trot, pairs, bw, n_plus,
                                                            inner, inner_limit, tol_c, counters, s);
+    else if (use_inner4)
+      launch_inner4(Hbuf, Vbuf, trot, pairs, ntask, w, n_plus, inner, inner_limit, tol_c,
+                    counters, s, st);
     else if (inner3_ok(w))
       launch_inner3(Hbuf, Vbuf, trot, pairs, ntask, w, n_plus, inner, inner_limit, tol_c,
                     counters, s, st);
