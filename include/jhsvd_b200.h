@@ -116,6 +116,12 @@ int jh_probe_rate(int kind, int ctas, int threads, int iters, double *out, void 
  * enables, 0 disables; out (host uint64[8]) receives and resets them. */
 int jh_inner_profile(int on, unsigned long long *out);
 
+/* Diagnostic / test: branch-free division and sqrt fast paths vs the IEEE
+ * operators on n operand pairs; cnt (device uint64[4]) += division
+ * mismatches, division rejections, sqrt mismatches, sqrt rejections. */
+int jh_probe_fastmath(const double *a, const double *b, int64_t n, unsigned long long *cnt,
+                      void *stream);
+
 /* Diagnostic: dependent-chain latencies (cycles/op) of DFMA, DMUL, division,
  * sqrt, the rotation formula and a shared-memory load; out[6]. */
 int jh_probe_latency(double *out, void *stream);

@@ -13,6 +13,7 @@
 // barrier ends the p-step.  Everything lives in shared memory with column
 // stride W + 1.
 #include "jh_common.cuh"
+#include "jh_fastmath.cuh"
 #include "jh_kernels.h"
 
 namespace jh {
@@ -509,9 +510,15 @@ k_factor_inner4(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
     }
     int64_t tot_rot = 0, tot_proper = 0;
     int gstep = 0, status = 0, bad = -1;
+    const bool prof = g_inner_prof_on != 0;
+    unsigned long long pt[4] = {0, 0, 0, 0};
+    long long c0 = 0, c1 = 0;
+    int nsw = 0;
     for (int sw = 0; sw < inner_limit && !status; sw++) {
       int a_r = 0, b_r = 0;
+      nsw++;
       for (int si = 0; si < NSTEP; si++, gstep++) {
+        if (prof) c0 = clock64();
         // dots: chains through the group's lanes in row order
         double hpp = 0.0, hqq = 0.0, hpq = 0.0;
 #pragma unroll
@@ -543,9 +550,21 @@ k_factor_inner4(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
           hqq = __shfl_sync(0xffffffffu, hqq, src);
           hpq = __shfl_sync(0xffffffffu, hpq, src);
         }
+        if (prof) {
+          c1 = clock64() + (long long)(hpp * 0.0 + hqq * 0.0 + hpq * 0.0);
+          pt[0] += c1 - c0;
+          c0 = c1;
+        }
         const bool hyp = S.sg[p] > 0 && S.sg[q] < 0;
-        double cs, tn;
-        const bool rot_ok = rotation_core_sel(hpp, hqq, hpq, hyp ? -1.0 : 1.0, cs, tn);
+        double cs, tn, sp, sq;
+        bool fast_ok;
+        bool rot_ok = rotation_core_fast(hpp, hqq, hpq, hyp ? -1.0 : 1.0, cs, tn, sp, sq, fast_ok);
+        if (__any_sync(0xffffffffu, !fast_ok)) {
+          // some operand left the fast paths' range: IEEE operators throughout
+          rot_ok = rotation_core_sel(hpp, hqq, hpq, hyp ? -1.0 : 1.0, cs, tn);
+          sp = sqrt(hpp);
+          sq = sqrt(hqq);
+        }
         int act = 0, fail = 0, fb = 0;
         if (hpp == 0.0) {
           fail = kZeroColumn;
@@ -553,7 +572,7 @@ k_factor_inner4(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
         } else if (hqq == 0.0) {
           fail = kZeroColumn;
           fb = q + 1;
-        } else if (!(fabs(hpq) < tol_c * sqrt(hpp) * sqrt(hqq))) {
+        } else if (!(fabs(hpq) < tol_c * sp * sq)) {
           if (!rot_ok) {
             fail = kHypDomain;
             fb = p + 1;
@@ -577,6 +596,11 @@ k_factor_inner4(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
           a_r++;
           if (cs != 1.0) b_r++;
         }
+        if (prof) {
+          c1 = clock64() + (long long)(cs * 0.0 + tn * 0.0);
+          pt[1] += c1 - c0;
+          c0 = c1;
+        }
         // publish for the V warp (ring slot free once V consumed step gstep - kRing)
         if (k == 0) {
           while (gstep - S.consumed >= kRing) {
@@ -591,6 +615,11 @@ k_factor_inner4(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
         if (lane == 0) {
           __threadfence_block();
           S.produced = gstep + 1;
+        }
+        if (prof) {
+          c1 = clock64();
+          pt[2] += c1 - c0;
+          c0 = c1;
         }
         // rotate my rows in registers
         if (act) {
@@ -623,6 +652,10 @@ k_factor_inner4(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
           cq[r] = S.R[q * LDR + r0 + r];
         }
         __syncwarp();
+        if (prof) {
+          c1 = clock64() + (long long)(cp[RPL - 1] * 0.0);
+          pt[3] += c1 - c0;
+        }
       }
       if (status) break;
       const int ta = __reduce_add_sync(0xffffffffu, a_r);
@@ -636,6 +669,12 @@ k_factor_inner4(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
       S.bad = bad;
       __threadfence_block();
       S.finished = 1;
+    }
+    if (prof && lane == 0) {
+      for (int j = 0; j < 4; j++) atomicAdd(&g_inner_prof[j], pt[j]);
+      atomicAdd(&g_inner_prof[5], (unsigned long long)gstep);
+      atomicAdd(&g_inner_prof[6], (unsigned long long)nsw);
+      atomicAdd(&g_inner_prof[7], 1ull);
     }
     if (lane == 0 && !status) {
       task_rot[task] = tot_rot;

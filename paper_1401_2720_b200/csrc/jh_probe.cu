@@ -146,3 +146,38 @@ extern "C" int jh_probe_latency(double *out, void *stream) {
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : -(int)e;
 }
+
+// Diagnostic / test: the branch-free fast paths (jh_fastmath.cuh) against the
+// IEEE operators.  cnt[0] = division mismatches on fast-ok lanes, cnt[1] =
+// division fast-path rejections, cnt[2] / cnt[3] the same for sqrt (of |a|).
+#include "jh_fastmath.cuh"
+namespace jh {
+__global__ void k_probe_fastmath(const double *__restrict__ a, const double *__restrict__ b,
+                                 int64_t n, unsigned long long *cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    bool ok = true;
+    const double q = div_fp(a[i], b[i], ok);
+    const double qi = a[i] / b[i];
+    if (!ok)
+      atomicAdd(&cnt[1], 1ull);
+    else if (__double_as_longlong(q) != __double_as_longlong(qi))
+      atomicAdd(&cnt[0], 1ull);
+    bool ok2 = true;
+    const double x = fabs(a[i]);
+    const double s = sqrt_fp(x, ok2);
+    const double si = sqrt(x);
+    if (!ok2)
+      atomicAdd(&cnt[3], 1ull);
+    else if (__double_as_longlong(s) != __double_as_longlong(si))
+      atomicAdd(&cnt[2], 1ull);
+  }
+}
+}  // namespace jh
+
+extern "C" int jh_probe_fastmath(const double *a, const double *b, int64_t n,
+                                 unsigned long long *cnt, void *stream) {
+  jh::k_probe_fastmath<<<1184, 256, 0, (cudaStream_t)stream>>>(a, b, n, cnt);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : -(int)e;
+}

@@ -87,7 +87,7 @@ def inner_profile(n=4096, w=32, steps=8):
     lib.jh_inner_profile(0, out)
     v = list(out)
     nst = max(v[5], 1)
-    names = ["dots", "rotation", "barrier1", "apply_R", "barrier2"]
+    names = ["dots", "rotation", "publish", "apply+exch", "(v3 bar2)"]
     print(f"inner profile n={n} w={w}: {v[7]} tasks, {v[6] / max(v[7], 1):.2f} inner sweeps/task, "
           f"{v[5] / max(v[7], 1):.1f} inner p-steps/task")
     tot = sum(v[:5]) / nst
