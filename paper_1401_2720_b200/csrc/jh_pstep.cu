@@ -748,6 +748,26 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
   const bool use_dmma_update = !force_simple && update_dmma_ok(w);
   static const char *env_inner = getenv("JHSVD_INNER");  // "3" selects the v3 kernel
   const bool use_inner4 = !force_simple && inner4_ok(w) && !(env_inner && env_inner[0] == '3');
+  // Default fast path: Gram kernel + fused (inner Jacobi -> post-multiply)
+  // kernel per p-step (JHSVD_FUSED=0 selects the three-kernel form).
+  static const char *env_fused = getenv("JHSVD_FUSED");
+  const bool fused = use_tma_gram && use_dmma_update && !(env_fused && env_fused[0] == '0') &&
+                     fused_ok(w, m, ldg, V ? nv : 0, V ? ldv : 0);
+  if (fused) {
+    for (int s = first_step; s < first_step + nsteps; s++) {
+      const int32_t *pairs = outer + (int64_t)s * ntask * 2;
+      prof_mark(st, 0, false);
+      launch_gram_tma(G, ldg, m, pairs, ntask, w, Hbuf, st);
+      prof_mark(st, 0, true);
+      prof_mark(st, 1, false);
+      launch_fused(G, ldg, m, V, ldv, nv, Hbuf, trot, pairs, ntask, w, n_plus, inner,
+                   inner_limit, tol_c, counters, s, st);
+      prof_mark(st, 1, true);
+      g_launches += 2;
+    }
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : -(int)e;
+  }
   // K-way staggered pipeline of a p-step (JHSVD_STREAMS = K, 0/1 disables)
   static const int env_k = [] {
     const char *e = getenv("JHSVD_STREAMS");
