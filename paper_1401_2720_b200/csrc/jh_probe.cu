@@ -5,6 +5,7 @@
 // (hard part H1).  Used by tests/ and the probe script;
 // not on the solver path.
 #include "jh_common.cuh"
+#include "jh_fastmath.cuh"
 
 namespace jh {
 
@@ -138,11 +139,31 @@ __global__ void k_latency(double seed, double *out) {
   for (int i = 0; i < N; i++) idx = chase[idx];
   t1 = clock64();
   out[5] = (double)(t1 - t0) / N + 0.0 * idx;
+  bool ok = true;
+  double d2 = seed + 2.0;
+  t0 = clock64();
+  for (int i = 0; i < N; i++) d2 = div_fp(3.0, d2, ok);
+  t1 = clock64();
+  out[6] = (double)(t1 - t0) / N + 0.0 * d2;
+  double s2 = seed + 3.0;
+  t0 = clock64();
+  for (int i = 0; i < N; i++) s2 = sqrt_fp(s2, ok) + 1.0;
+  t1 = clock64();
+  out[7] = (double)(t1 - t0) / N + 0.0 * s2;
+  double h2 = 0.3 + seed, c2, tn2, sp, sq;
+  bool okf;
+  t0 = clock64();
+  for (int i = 0; i < N; i++) {
+    rotation_core_fast(1.5, 1.0, h2, 1.0, c2, tn2, sp, sq, okf);
+    h2 = 0.3 + tn2 * 1e-9;
+  }
+  t1 = clock64();
+  out[8] = (double)(t1 - t0) / N + 0.0 * c2 + (ok && okf ? 0.0 : 1e9);
 }
 }  // namespace jh
 
 extern "C" int jh_probe_latency(double *out, void *stream) {
-  jh::k_latency<<<1, 32, 0, (cudaStream_t)stream>>>(0.5, out);
+  jh::k_latency<<<1, 32, 0, (cudaStream_t)stream>>>(0.5, out);  // out[0..8]
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : -(int)e;
 }

@@ -748,10 +748,12 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
   const bool use_dmma_update = !force_simple && update_dmma_ok(w);
   static const char *env_inner = getenv("JHSVD_INNER");  // "3" selects the v3 kernel
   const bool use_inner4 = !force_simple && inner4_ok(w) && !(env_inner && env_inner[0] == '3');
-  // Default fast path: Gram kernel + fused (inner Jacobi -> post-multiply)
-  // kernel per p-step (JHSVD_FUSED=0 selects the three-kernel form).
+  // Optional: Gram kernel + fused (inner Jacobi -> post-multiply) kernel per
+  // p-step (JHSVD_FUSED=1).
   static const char *env_fused = getenv("JHSVD_FUSED");
-  const bool fused = use_tma_gram && use_dmma_update && !(env_fused && env_fused[0] == '0') &&
+  // (off by default: per task the update is confined to one SM, which makes
+  // the DMMA work per SM uneven; measured slower than the three kernels)
+  const bool fused = use_tma_gram && use_dmma_update && (env_fused && env_fused[0] == '1') &&
                      fused_ok(w, m, ldg, V ? nv : 0, V ? ldv : 0);
   if (fused) {
     for (int s = first_step; s < first_step + nsteps; s++) {

@@ -40,11 +40,12 @@ if __name__ == "__main__" and "--latency" not in sys.argv:
 
 def latency():
     lib = _lib.require_cuda()
-    out = torch.zeros(6, dtype=torch.float64, device="cuda")
+    out = torch.zeros(9, dtype=torch.float64, device="cuda")
     for _ in range(2):
         _lib.check(lib.jh_probe_latency(out.data_ptr(), _lib.stream_handle()), "lat")
         torch.cuda.synchronize()
-    names = ["dfma", "dmul", "ddiv", "dsqrt", "rotation_core", "lds"]
+    names = ["dfma", "dmul", "ddiv", "dsqrt", "rotation_core", "lds", "div_fp", "sqrt_fp",
+             "rotation_core_fast"]
     r = dict(zip(names, out.cpu().tolist()))
     print(json.dumps({"latency_cycles": r}))
     return r
