@@ -122,6 +122,12 @@ int jh_inner_profile(int on, unsigned long long *out);
 int jh_probe_fastmath(const double *a, const double *b, int64_t n, unsigned long long *cnt,
                       void *stream);
 
+/* Diagnostic: launch inner-Jacobi kernel variant 3, 4 or 5 on the Gram
+ * matrices in Hbuf (A/B timing, tools/bench_inner.py). */
+int jh_bench_inner(int variant, const double *Hbuf, double *Vbuf, int64_t *trot,
+                   const int32_t *pairs, int ntask, int w, int64_t n_plus, const int32_t *inner,
+                   int inner_limit, double tol_c, unsigned long long *counters, void *stream);
+
 /* Diagnostic: dependent-chain latencies (cycles/op) of DFMA, DMUL, division,
  * sqrt, the rotation formula and a shared-memory load; out[6]. */
 int jh_probe_latency(double *out, void *stream);

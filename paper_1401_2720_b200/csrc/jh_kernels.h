@@ -38,4 +38,10 @@ void launch_fused(double *G, int64_t ldg, int64_t m, double *V, int64_t ldv, int
                   int64_t n_plus, const int32_t *inner, int inner_limit, double tol_c,
                   unsigned long long *counters, int pstep, cudaStream_t st, int task_base = 0);
 
+// the first v3 inner Jacobi, kept for A/B timing (jh_inner5.cu)
+bool inner5_ok(int w);
+void launch_inner5(const double *Hbuf, double *Vbuf, int64_t *trot, const int32_t *pairs,
+                   int ntask, int w, int64_t n_plus, const int32_t *inner, int inner_limit,
+                   double tol_c, unsigned long long *counters, int pstep, cudaStream_t st);
+
 }  // namespace jh
