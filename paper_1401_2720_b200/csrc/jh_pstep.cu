@@ -746,8 +746,38 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
   static const bool force_simple = getenv("JHSVD_FORCE_SIMPLE") != nullptr;
   const bool use_tma_gram = !force_simple && gram_tma_ok(w, m, ldg);
   const bool use_dmma_update = !force_simple && update_dmma_ok(w);
-  static const char *env_inner = getenv("JHSVD_INNER");  // "3" selects the v3 kernel
-  const bool use_inner4 = !force_simple && inner4_ok(w) && !(env_inner && env_inner[0] == '3');
+  // inner-Jacobi kernel variant: 5 (default; fastest at n = 16384 in
+  // tools/bench_inner.py), 4 (register-resident R), 3 (batched applies)
+  static const int inner_variant = [] {
+    const char *e = getenv("JHSVD_INNER");
+    return e ? atoi(e) : 5;
+  }();
+  const bool use_inner4 = !force_simple && inner4_ok(w) && inner_variant == 4;
+  if (!force_simple && inner_variant == 5 && inner5_ok(w)) {
+    for (int s = first_step; s < first_step + nsteps; s++) {
+      const int32_t *pairs = outer + (int64_t)s * ntask * 2;
+      prof_mark(st, 0, false);
+      if (use_tma_gram)
+        launch_gram_tma(G, ldg, m, pairs, ntask, w, Hbuf, st);
+      else
+        k_gram<<<ntask, kGramThreads, smem_gram, st>>>(G, ldg, m, pairs, bw, Hbuf);
+      prof_mark(st, 0, true);
+      prof_mark(st, 1, false);
+      launch_inner5(Hbuf, Vbuf, trot, pairs, ntask, w, n_plus, inner, inner_limit, tol_c, counters,
+                    s, st);
+      prof_mark(st, 1, true);
+      prof_mark(st, 2, false);
+      if (use_dmma_update)
+        launch_update_dmma(G, ldg, m, V, ldv, nv, pairs, ntask, w, Vbuf, trot, st);
+      else
+        k_update<<<dim3(ntask, nbg + nbv), kUpdThreads, smem_upd, st>>>(
+            G, ldg, m, V, ldv, nv, pairs, bw, Vbuf, trot, nbg);
+      prof_mark(st, 2, true);
+      g_launches += 3;
+    }
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : -(int)e;
+  }
   // Optional: Gram kernel + fused (inner Jacobi -> post-multiply) kernel per
   // p-step (JHSVD_FUSED=1).
   static const char *env_fused = getenv("JHSVD_FUSED");
