@@ -302,13 +302,19 @@ def run_ours(args, rank: int, world: int):
     dom = max(("gram", "update"), key=lambda k: classes[k]["ms"])
     d = classes[dom]
     achieved = d["bytes_total"] / (d["ms"] / 1e3) / 1e9 if d["ms"] > 0 else 0.0
-    traffic = None
+    # DRAM traffic of the same kernel from one `ncu --set full` capture
+    # (profiles/ncu_traffic.json: one launch with every task rotating, with the
+    # algorithmic bytes of that launch for comparison)
+    traffic = traffic_alg = None
     tp = ROOT / "profiles" / "ncu_traffic.json"
     if tp.exists():
-        traffic = json.loads(tp.read_text()).get(dom)
+        tj = json.loads(tp.read_text())
+        traffic = tj.get(dom)
+        traffic_alg = tj.get(dom + "_algorithmic")
     roofline = {
         "kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
         "frac": achieved / hbm_peak, "traffic": traffic,
+        "traffic_launch_algorithmic_bytes": traffic_alg,
         "bytes_per_launch": d["bytes_total"] / max(d["launches"], 1),
         "avg_launch_ms": d["ms"] / max(d["launches"], 1),
         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
