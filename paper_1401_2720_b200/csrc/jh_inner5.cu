@@ -2,54 +2,10 @@
 // written -- one CTA of 4 warps per task, pairs' dot products by w/2 lanes of
 // warp 0, R applied by all threads one pair at a time, V applied by warps 1-3
 // one inner p-step behind.  Same arithmetic as every other variant.
-#include "jh_common.cuh"
+#include "jh_inner5.cuh"
 #include "jh_kernels.h"
 
 namespace jh {
-
-template <int W>
-struct InnerCfg5 {
-  static constexpr int HALF = W / 2;
-  static constexpr int LD = W + 1;
-  static constexpr int NTH = W <= 32 ? 128 : 256;
-};
-
-struct StepParams5 {
-  double cs, tn;
-  int act;  // 0 skip, 1 rotate, 2 rotate + swap, 4 | 1 hyperbolic rotate
-};
-
-template <int W>
-struct InnerSmem5 {
-  double H[W * W];
-  double R[W * (W + 1)];
-  double V[W * (W + 1)];
-  StepParams5 prm[2][W / 2];
-  int8_t steps[(W - 1) * W];  // (p, q) per pair per inner p-step
-  int8_t sg[W];
-  int fail_status, fail_bad, stop, sweep_rot, sweep_proper, chol;
-};
-
-// rotate (+ swap) columns p, q of M (ld LD) at row i
-__device__ __forceinline__ void rot_apply5(double *M, int ld, int p, int q, int i,
-                                          const StepParams5 &pr) {
-  const double cs = pr.cs, tn = pr.tn;
-  const double s = (pr.act & 4) ? tn : -tn;
-  double *mp = M + p * ld + i, *mq = M + q * ld + i;
-  const double gp = *mp, gq = *mq;
-  double np = fma(s, gq, gp), nq = fma(tn, gp, gq);
-  if (cs != 1.0) {
-    np = np * cs;
-    nq = nq * cs;
-  }
-  if ((pr.act & 3) == 2) {
-    *mp = nq;
-    *mq = np;
-  } else {
-    *mp = np;
-    *mq = nq;
-  }
-}
 
 template <int W>
 __global__ void __launch_bounds__(InnerCfg5<W>::NTH)
@@ -57,203 +13,11 @@ k_factor_inner5(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
                 int64_t *__restrict__ task_rot, const int32_t *__restrict__ pairs,
                 int64_t n_plus, const int32_t *__restrict__ inner, int inner_limit,
                 double tol_c, unsigned long long *counters, int pstep) {
-  constexpr int HALF = InnerCfg5<W>::HALF, LD = InnerCfg5<W>::LD, NTH = InnerCfg5<W>::NTH;
-  constexpr int BW = W / 2, NSTEP = W - 1;
   extern __shared__ __align__(16) unsigned char smraw[];
-  InnerSmem5<W> &S = *reinterpret_cast<InnerSmem5<W> *>(smraw);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int task = blockIdx.x;
-  const int p0 = pairs[2 * task], q0 = pairs[2 * task + 1];
-
-  // ---- load H, inner table, signs; V = I
-  const double *Hg = Hbuf + (size_t)task * W * W;
-  for (int i = tid; i < W * W; i += NTH) S.H[i] = Hg[i];
-  for (int i = tid; i < W * LD; i += NTH) {
-    const int col = i / LD, row = i - col * LD;
-    S.V[i] = (row == col) ? 1.0 : 0.0;
-  }
-  for (int i = tid; i < NSTEP * W; i += NTH) S.steps[i] = (int8_t)inner[i];
-  for (int j = tid; j < W; j += NTH) {
-    const int64_t gcol = (j < BW ? (int64_t)p0 * BW + j : (int64_t)q0 * BW + (j - BW)) + 1;
-    S.sg[j] = gcol <= n_plus ? 1 : -1;
-  }
-  if (tid == 0) {
-    S.chol = 0;
-    S.stop = 0;
-  }
-  __syncthreads();
-
-  // ---- forward-looking Cholesky (reference element order), lower triangle
-  {
-    const int x = tid % W, jg = tid / W;
-    constexpr int JS = NTH / W;
-    for (int k = 0; k < W; k++) {
-      if (tid == 0) {
-        const double d = S.H[k * W + k];
-        if (!(d > 0.0) || !isfinite(d))
-          S.chol = k + 1;
-        else
-          S.H[k * W + k] = sqrt(d);
-      }
-      __syncthreads();
-      if (S.chol) break;
-      const double l = S.H[k * W + k];
-      if (jg == 0 && x > k) S.H[k * W + x] = S.H[k * W + x] / l;
-      __syncthreads();
-      for (int j = k + 1 + jg; j < W; j += JS)
-        if (x >= j) S.H[j * W + x] = fma(-S.H[k * W + x], S.H[k * W + j], S.H[j * W + x]);
-      __syncthreads();
-    }
-  }
-  if (S.chol) {
-    if (tid == 0) {
-      task_rot[task] = 0;
-      atomicMin(&counters[2], err_key(pstep, task, kCholesky, S.chol));
-    }
-    return;
-  }
-  // R = L^T (R[i][j] = H[i * W + j] for i <= j)
-  for (int e = tid; e < W * W; e += NTH) {
-    const int j = e / W, i = e - j * W;
-    S.R[j * LD + i] = (i <= j) ? S.H[i * W + j] : 0.0;
-  }
-  __syncthreads();
-
-  // ---- inner sweeps
-  int a_r = 0, b_r = 0;  // lane-private counters of warp 0
-  int64_t tot_rot = 0, tot_proper = 0;
-  int sweeps = 0, status = 0, bad = -1;
-  int gstep = 0;  // global inner p-step counter (for the lagged V update)
-  const int ri = tid % W;         // row handled in the R / V applies
-  const int rg = tid / W;         // pair group
-  constexpr int RGS = NTH / W;    // pair groups in the R apply
-  for (int sw = 0; sw < inner_limit && !status; sw++) {
-    for (int si = 0; si < NSTEP; si++, gstep++) {
-      const int8_t *st = S.steps + si * W;
-      StepParams5 *cur = S.prm[gstep & 1];
-      if (warp == 0) {
-        int fail = 0, fb = 0;
-        if (lane < HALF) {
-          const int p = st[2 * lane], q = st[2 * lane + 1];
-          const double *cp = S.R + p * LD, *cq = S.R + q * LD;
-          double hpp = 0.0, hqq = 0.0, hpq = 0.0;
-#pragma unroll
-          for (int i = 0; i < W; i++) {
-            const double gp = cp[i], gq = cq[i];
-            hpp = fma(gp, gp, hpp);
-            hqq = fma(gq, gq, hqq);
-            hpq = fma(gp, gq, hpq);
-          }
-          StepParams5 pr{1.0, 0.0, 0};
-          // the rotation is formed speculatively, in parallel with the
-          // orthogonality test (it has no side effects; a pair that passes
-          // the test discards it, exactly like the reference never forms it)
-          const bool hyp = S.sg[p] > 0 && S.sg[q] < 0;
-          double cs, tn;
-          const bool rot_ok = rotation_core(hpp, hqq, hpq, hyp ? -1.0 : 1.0, cs, tn);
-          if (hpp == 0.0) {
-            fail = kZeroColumn;
-            fb = p + 1;
-          } else if (hqq == 0.0) {
-            fail = kZeroColumn;
-            fb = q + 1;
-          } else if (!(fabs(hpq) < tol_c * sqrt(hpp) * sqrt(hqq))) {
-            if (!rot_ok) {
-              fail = kHypDomain;
-              fb = p + 1;
-            } else {
-              a_r++;
-              if (cs != 1.0) b_r++;
-              pr.cs = cs;
-              pr.tn = tn;
-              pr.act = hyp ? 5 : 1;
-              if (!hyp) {
-                const double h1 = fma(-tn, hpq, hpp);
-                const double h2 = fma(tn, hpq, hqq);
-                if ((S.sg[p] > 0 && h1 < h2) || (S.sg[p] < 0 && h1 > h2)) pr.act = 2;
-              }
-            }
-          }
-          cur[lane] = pr;
-        }
-        const unsigned fm = __ballot_sync(0xffffffffu, fail != 0);
-        if (fm) {
-          const int first = __ffs(fm) - 1;  // first failing pair in reference order
-          const int fs = __shfl_sync(0xffffffffu, fail, first);
-          const int fbb = __shfl_sync(0xffffffffu, fb, first);
-          if (lane == 0) {
-            S.fail_status = fs;
-            S.fail_bad = fbb;
-            S.stop = 1;
-          }
-        }
-      } else if (gstep > 0) {
-        // lagged V update of the previous inner p-step (warps 1..)
-        const int8_t *pst = S.steps + ((si + NSTEP - 1) % NSTEP) * W;
-        const StepParams5 *prev = S.prm[(gstep - 1) & 1];
-        const int vt = tid - 32, vrow = vt % W, vg = vt / W;
-        constexpr int VGS = (NTH - 32) / W;
-        if (vt < VGS * W)
-          for (int pi = vg; pi < HALF; pi += VGS)
-            if (prev[pi].act) rot_apply5(S.V, LD, pst[2 * pi], pst[2 * pi + 1], vrow, prev[pi]);
-      }
-      __syncthreads();
-      if (S.stop) {
-        status = S.fail_status;
-        bad = S.fail_bad;
-        break;
-      }
-      // R update of this inner p-step (all threads)
-      for (int pi = rg; pi < HALF; pi += RGS)
-        if (cur[pi].act) rot_apply5(S.R, LD, st[2 * pi], st[2 * pi + 1], ri, cur[pi]);
-      __syncthreads();
-    }
-    if (status) break;
-    // sweep end: totals of applied / proper rotations
-    if (warp == 0) {
-      const int ta = __reduce_add_sync(0xffffffffu, a_r);
-      const int tb = __reduce_add_sync(0xffffffffu, b_r);
-      a_r = b_r = 0;
-      if (lane == 0) {
-        S.sweep_rot = ta;
-        S.sweep_proper = tb;
-      }
-    }
-    __syncthreads();
-    const int ta = S.sweep_rot, tb = S.sweep_proper;
-    __syncthreads();
-    sweeps++;
-    tot_rot += ta;
-    tot_proper += tb;
-    if (ta == 0) break;
-  }
-  if (status) {
-    if (tid == 0) {
-      task_rot[task] = 0;
-      atomicMin(&counters[2], err_key(pstep, task, status, bad));
-    }
-    return;
-  }
-  // flush the lagged V update of the last inner p-step
-  if (gstep > 0) {
-    const int last = (gstep - 1) % NSTEP;
-    const int8_t *pst = S.steps + last * W;
-    const StepParams5 *prev = S.prm[(gstep - 1) & 1];
-    for (int pi = rg; pi < HALF; pi += RGS)
-      if (prev[pi].act) rot_apply5(S.V, LD, pst[2 * pi], pst[2 * pi + 1], ri, prev[pi]);
-  }
-  __syncthreads();
-  double *Vg = Vbuf + (size_t)task * W * W;
-  for (int e = tid; e < W * W; e += NTH) {
-    const int j = e / W, i = e - j * W;
-    Vg[e] = S.V[j * LD + i];
-  }
-  if (tid == 0) {
-    task_rot[task] = tot_rot;
-    atomicAdd(&counters[0], (unsigned long long)tot_rot);
-    atomicAdd(&counters[1], (unsigned long long)tot_proper);
-    if (tot_rot) atomicAdd(&counters[3], 1ull);
-  }
+  inner5_task<W, InnerCfg5<W>::NTH>(smraw, Hbuf + (size_t)task * W * W, Vbuf + (size_t)task * W * W,
+                                    pairs[2 * task], pairs[2 * task + 1], n_plus, inner,
+                                    inner_limit, tol_c, counters, pstep, task, &task_rot[task]);
 }
 
 bool inner5_ok(int w) { return w == 16 || w == 32 || w == 64; }
