@@ -680,11 +680,11 @@ int jh_profile_begin(int max_launches) {
 }
 
 // Stop timing; synchronizes on the recorded events and returns per kernel
-// class (0 gram, 1 factor+inner, 2 update) the summed milliseconds and the
-// number of timed launches.
+// class (0 gram, 1 factor+inner, 2 update, 3 dataflow sweep kernel) the
+// summed milliseconds and the number of timed launches (arrays of 4).
 int jh_profile_end(double *ms, int64_t *count) {
   g_prof.on = false;
-  for (int k = 0; k < 3; k++) {
+  for (int k = 0; k < 4; k++) {
     ms[k] = 0.0;
     count[k] = 0;
   }
@@ -701,7 +701,13 @@ int jh_profile_end(double *ms, int64_t *count) {
 // Bytes of device workspace jh_block_sweep needs for order n and width w.
 int64_t jh_sweep_workspace_bytes(int64_t n, int w) {
   const int64_t ntask = n / w;  // b/2 with b = n / (w/2)
-  return ntask * (int64_t)w * w * 8 * 2 + ntask * 8 + 256;
+  const int64_t base = ntask * (int64_t)w * w * 8 * 2 + ntask * 8 + 256;
+  if (w == 16 || w == 32) {
+    // + the dataflow path's per-(p-step, task) scratch for a whole sweep
+    const int nsteps = (int)(n / (w / 2)) - 1;
+    return base + dataflow_workspace_bytes(n, w, nsteps);
+  }
+  return base;
 }
 
 // One block sweep (or p-steps [first_step, first_step + nsteps) of it) of
@@ -746,6 +752,21 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
   static const bool force_simple = getenv("JHSVD_FORCE_SIMPLE") != nullptr;
   const bool use_tma_gram = !force_simple && gram_tma_ok(w, m, ldg);
   const bool use_dmma_update = !force_simple && update_dmma_ok(w);
+  // Default: dataflow execution of the requested p-steps in one persistent
+  // kernel (jh_dataflow.cu); JHSVD_DATAFLOW=0 selects the per-p-step kernels.
+  if (!force_simple && use_tma_gram && use_dmma_update &&
+      dataflow_ok(w, m, ldg, V ? nv : 0, V ? ldv : 0)) {
+    const int64_t base = (int64_t)ntask * w * w * 8 * 2 + (int64_t)ntask * 8 + 256;
+    const int nsteps_total = (int)(n / bw) - 1;
+    prof_mark(st, 3, false);
+    launch_dataflow(G, ldg, m, V, ldv, nv, w, outer, first_step, first_step + nsteps,
+                    nsteps_total, inner, n_plus, inner_limit, tol_c, counters,
+                    (char *)workspace + base, n, st);
+    prof_mark(st, 3, true);
+    g_launches += 3;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : -(int)e;
+  }
   // inner-Jacobi kernel variant: 5 (default; fastest at n = 16384 in
   // tools/bench_inner.py), 4 (register-resident R), 3 (batched applies)
   static const int inner_variant = [] {

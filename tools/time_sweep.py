@@ -45,15 +45,17 @@ def main():
         ms = e0.elapsed_time(e1)
         ns = steps or eng.nsteps
         rot, proper, key, nrot = c.cpu().tolist()
-        pms = (ctypes.c_double * 3)()
-        pcnt = (ctypes.c_int64 * 3)()
+        pms = (ctypes.c_double * 4)()
+        pcnt = (ctypes.c_int64 * 4)()
         lib.jh_profile_end(pms, pcnt)
         print(f"n={n} w={w} sweep {s}: {ms:.1f} ms for {ns} p-steps "
               f"({ms / ns:.3f} ms/p-step) rot={rot} proper={proper} key={key} "
               f"rotated_tasks={nrot}", flush=True)
-        names = ("gram", "factor_inner", "update")
+        names = ("gram", "factor_inner", "update", "dataflow")
         ntask = n // w
-        for k in range(3):
+        for k in range(4):
+            if pcnt[k] == 0:
+                continue
             per = pms[k] / max(pcnt[k], 1)
             extra = ""
             if k == 0:
@@ -62,6 +64,10 @@ def main():
             if k == 2:
                 gbs = nrot * 16.0 * w * 2 * n / (pms[k] / 1e3) / 1e9
                 extra = f" {gbs:.0f} GB/s"
+            if k == 3:
+                nst = steps or eng.nsteps
+                byts = nst * ntask * 8.0 * w * n + nrot * 16.0 * w * 2 * n
+                extra = f" {byts / (pms[k] / 1e3) / 1e9:.0f} GB/s (Gram + update bytes)"
             print(f"   {names[k]:13s} {pms[k]:9.2f} ms total, {per * 1e3:9.1f} us/launch{extra}")
 
 
