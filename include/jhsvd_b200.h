@@ -55,6 +55,31 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
                    void *workspace, int64_t ws_bytes, unsigned long long *counters,
                    void *stream);
 
+/*
+ * Cycle engine (the default sweep path for w = 32 on pivot tables whose
+ * consecutive p-steps pair the block-columns in 4-cycles, e.g. rrow):
+ * jh_cycle_plan (host) checks the structure of a host pivot table
+ * int32[b-1][b/2][2] and fills plan[jh_cycle_plan_ints(b)] (0 = usable,
+ * 1 = not usable); jh_block_sweep_cycle then runs the same p-steps as
+ * jh_block_sweep -- bitwise the same G, V and counters -- as one persistent
+ * kernel in which the post-multiplication of p-step s-1 and the Gram of
+ * p-step s share one pass over G, and V is updated two p-steps per pass.
+ * plan is the device copy; NULL (or w != 32) falls back to jh_block_sweep.
+ * Same reference functions as jh_block_sweep (driver.py:153-190).
+ */
+int64_t jh_cycle_plan_ints(int b);
+int jh_cycle_plan(const int32_t *outer, int b, int32_t *plan);
+int jh_block_sweep_cycle(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int64_t ldv,
+                         int64_t nv, int w, const int32_t *outer, const int32_t *plan,
+                         int first_step, int nsteps, const int32_t *inner, int64_t n_plus,
+                         int inner_limit, double tol_c, void *workspace, int64_t ws_bytes,
+                         unsigned long long *counters, void *stream);
+
+/* Diagnostic: per-work-item trace of the cycle engine, records {item,
+ * smid, start ns, end ns} (int64) into device buf[4 + 4 cap], buf[0] =
+ * count; NULL disables. */
+int jh_cycle_trace(void *buf, int64_t cap);
+
 /* gram (blockkernel.py:99-107): H = A^T A, A m x c. */
 int jh_gram(const double *A, int64_t lda, int64_t m, int c, double *H, void *stream);
 
@@ -97,8 +122,8 @@ int jh_sigma_u(const double *G, int64_t ldg, int64_t m, int64_t n, double *sigma
                int64_t ldu, unsigned long long *bad, void *stream);
 
 /* Launch accounting / per-kernel-class timing (bench.py): classes are
- * 0 Gram, 1 factor + inner Jacobi, 2 update.  jh_profile_end synchronizes
- * on the recorded events. */
+ * 0 Gram, 1 factor + inner Jacobi, 2 update, 3 cycle-engine sweep kernel
+ * (arrays of 4).  jh_profile_end synchronizes on the recorded events. */
 unsigned long long jh_launch_count(void);
 int jh_profile_begin(int max_launches);
 int jh_profile_end(double *ms, int64_t *count);

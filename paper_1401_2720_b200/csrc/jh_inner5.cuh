@@ -70,7 +70,7 @@ __device__ __noinline__ long long inner5_task(unsigned char *smem, const double 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   // ---- load H, inner table, signs; V = I
-  for (int i = tid; i < W * W; i += NTH) S.H[i] = Hg[i];
+  for (int i = tid; i < W * W; i += NTH) S.H[i] = __ldcg(Hg + i);  // L2: produced this launch
   for (int i = tid; i < W * LD; i += NTH) {
     const int col = i / LD, row = i - col * LD;
     S.V[i] = (row == col) ? 1.0 : 0.0;

@@ -44,13 +44,17 @@ void launch_inner5(const double *Hbuf, double *Vbuf, int64_t *trot, const int32_
                    int ntask, int w, int64_t n_plus, const int32_t *inner, int inner_limit,
                    double tol_c, unsigned long long *counters, int pstep, cudaStream_t st);
 
-// dataflow execution of p-steps [s_begin, s_end) in one persistent kernel
-// (jh_dataflow.cu); ws = dataflow_workspace_bytes(n, w, nsteps_total) bytes
-bool dataflow_ok(int w, int64_t m, int64_t ldg, int64_t nv, int64_t ldv);
-int64_t dataflow_workspace_bytes(int64_t n, int w, int nsteps_total);
-int launch_dataflow(double *G, int64_t ldg, int64_t m, double *V, int64_t ldv, int64_t nv, int w,
-                    const int32_t *outer, int s_begin, int s_end, int nsteps_total,
-                    const int32_t *inner, int64_t n_plus, int inner_limit, double tol_c,
-                    unsigned long long *counters, void *ws, int64_t n, cudaStream_t st);
+// cycle engine (jh_cycle.cu): p-steps [s_begin, s_begin + nsteps) of one
+// sweep in one persistent kernel, w = 32, pivot tables with the 4-cycle
+// structure of consecutive p-steps (plan from cycle_plan)
+int64_t cycle_plan_ints(int b);
+int cycle_plan(const int32_t *outer, int b, int32_t *plan);
+bool cycle_ok(int w, int64_t m, int64_t ldg, int64_t nv, int64_t ldv);
+int64_t cycle_workspace_bytes(int64_t n, int w);
+void cycle_trace(void *buf, int64_t cap);
+int launch_cycle(double *G, int64_t ldg, int64_t m, double *V, int64_t ldv, int64_t nv,
+                 const int32_t *outer, const int32_t *plan, int b, int s_begin, int nsteps,
+                 const int32_t *inner, int64_t n_plus, int inner_limit, double tol_c,
+                 unsigned long long *counters, void *ws, cudaStream_t st);
 
 }  // namespace jh

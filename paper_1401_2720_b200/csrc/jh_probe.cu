@@ -83,15 +83,87 @@ __global__ void k_rate_dfma(int iters, double *out) {
   for (int i = 0; i < 8; i++) s += d[i];
   if (s == 12345.0) out[0] = s;
 }
+// DMMA with C independent chains per warp (latency probe)
+template <int C>
+__global__ void k_rate_dmma_c(int iters, double *out) {
+  const int lane = threadIdx.x & 31;
+  double a = 1.0 + lane * 1e-3, b = 1.0 - lane * 1e-3;
+  double d[C][2];
+#pragma unroll
+  for (int i = 0; i < C; i++) d[i][0] = d[i][1] = 0.0;
+  for (int it = 0; it < iters * 8 / C; it++) {
+#pragma unroll
+    for (int i = 0; i < C; i++)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(d[i][0]), "+d"(d[i][1])
+                   : "d"(a), "d"(b));
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < C; i++) s += d[i][0] + d[i][1];
+  if (s == 12345.0) out[0] = s;
+}
+
+// warps 0-3 (mod 8) DMMA, 4-7 DFMA: with 8 warps per CTA every SMSP runs
+// one of each (do the two FP64 paths add up?)
+__global__ void k_rate_mixed(int iters, double *out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double a = 1.0 + lane * 1e-3, b = 1.0 - lane * 1e-3;
+  double s = 0.0;
+  if (((warp >> 2) & 1) == 0) {
+    double d[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; i++) d[i][0] = d[i][1] = 0.0;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+      for (int i = 0; i < 8; i++)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(d[i][0]), "+d"(d[i][1])
+                     : "d"(a), "d"(b));
+    }
+#pragma unroll
+    for (int i = 0; i < 8; i++) s += d[i][0] + d[i][1];
+  } else {
+    double d[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) d[i] = i;
+    // 8x the DFMA iterations so both halves run about as long
+    for (int it = 0; it < 8 * iters; it++) {
+#pragma unroll
+      for (int i = 0; i < 8; i++) d[i] = fma(a, b, d[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; i++) s += d[i];
+  }
+  if (s == 12345.0) out[0] = s;
+}
 }  // namespace jh
 
 // FMAs executed = ctas * threads/32 * iters * 8 * (256 for DMMA, 32 for DFMA)
+// kind 2 (mixed): half the warps DMMA (iters * 8 * 256), half DFMA
+// (8 iters * 8 * 32): the same FMA count per warp.  kind 10 + C: DMMA with C
+// chains per warp (C in 1, 2, 4, 8, 16), same FMA count as kind 0.
 extern "C" int jh_probe_rate(int kind, int ctas, int threads, int iters, double *out,
                              void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
   if (kind == 0)
-    jh::k_rate_dmma<<<ctas, threads, 0, (cudaStream_t)stream>>>(iters, out);
+    jh::k_rate_dmma<<<ctas, threads, 0, st>>>(iters, out);
+  else if (kind == 1)
+    jh::k_rate_dfma<<<ctas, threads, 0, st>>>(iters, out);
+  else if (kind == 2)
+    jh::k_rate_mixed<<<ctas, threads, 0, st>>>(iters, out);
+  else if (kind == 11)
+    jh::k_rate_dmma_c<1><<<ctas, threads, 0, st>>>(iters, out);
+  else if (kind == 12)
+    jh::k_rate_dmma_c<2><<<ctas, threads, 0, st>>>(iters, out);
+  else if (kind == 14)
+    jh::k_rate_dmma_c<4><<<ctas, threads, 0, st>>>(iters, out);
+  else if (kind == 18)
+    jh::k_rate_dmma_c<8><<<ctas, threads, 0, st>>>(iters, out);
+  else if (kind == 26)
+    jh::k_rate_dmma_c<16><<<ctas, threads, 0, st>>>(iters, out);
   else
-    jh::k_rate_dfma<<<ctas, threads, 0, (cudaStream_t)stream>>>(iters, out);
+    return -1000;
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : -(int)e;
 }

@@ -680,7 +680,7 @@ int jh_profile_begin(int max_launches) {
 }
 
 // Stop timing; synchronizes on the recorded events and returns per kernel
-// class (0 gram, 1 factor+inner, 2 update, 3 dataflow sweep kernel) the
+// class (0 gram, 1 factor+inner, 2 update, 3 cycle-engine sweep kernel) the
 // summed milliseconds and the number of timed launches (arrays of 4).
 int jh_profile_end(double *ms, int64_t *count) {
   g_prof.on = false;
@@ -698,17 +698,22 @@ int jh_profile_end(double *ms, int64_t *count) {
   return 0;
 }
 
-// Bytes of device workspace jh_block_sweep needs for order n and width w.
+// Bytes of device workspace jh_block_sweep / jh_block_sweep_cycle need for
+// order n and width w.
 int64_t jh_sweep_workspace_bytes(int64_t n, int w) {
   const int64_t ntask = n / w;  // b/2 with b = n / (w/2)
   const int64_t base = ntask * (int64_t)w * w * 8 * 2 + ntask * 8 + 256;
-  if (w == 16 || w == 32) {
-    // + the dataflow path's per-(p-step, task) scratch for a whole sweep
-    const int nsteps = (int)(n / (w / 2)) - 1;
-    return base + dataflow_workspace_bytes(n, w, nsteps);
-  }
-  return base;
+  return base + cycle_workspace_bytes(n, w);
 }
+
+// Number of int32 entries of the cycle plan of a pivot table of order b
+// (0: order not supported by the cycle engine).
+int64_t jh_cycle_plan_ints(int b) { return cycle_plan_ints(b); }
+
+// Cycle plan of a host pivot table (int32[b-1][b/2][2], 0-based): 0 when
+// every pair of consecutive p-steps (with wrap) pairs the block-columns in
+// 4-cycles, so jh_block_sweep_cycle can fuse them; 1 otherwise.
+int jh_cycle_plan(const int32_t *outer, int b, int32_t *plan) { return cycle_plan(outer, b, plan); }
 
 // One block sweep (or p-steps [first_step, first_step + nsteps) of it) of
 // run_block_jacobi_inplace (driver.py:180-190) on device data.
@@ -752,21 +757,6 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
   static const bool force_simple = getenv("JHSVD_FORCE_SIMPLE") != nullptr;
   const bool use_tma_gram = !force_simple && gram_tma_ok(w, m, ldg);
   const bool use_dmma_update = !force_simple && update_dmma_ok(w);
-  // Default: dataflow execution of the requested p-steps in one persistent
-  // kernel (jh_dataflow.cu); JHSVD_DATAFLOW=0 selects the per-p-step kernels.
-  if (!force_simple && use_tma_gram && use_dmma_update &&
-      dataflow_ok(w, m, ldg, V ? nv : 0, V ? ldv : 0)) {
-    const int64_t base = (int64_t)ntask * w * w * 8 * 2 + (int64_t)ntask * 8 + 256;
-    const int nsteps_total = (int)(n / bw) - 1;
-    prof_mark(st, 3, false);
-    launch_dataflow(G, ldg, m, V, ldv, nv, w, outer, first_step, first_step + nsteps,
-                    nsteps_total, inner, n_plus, inner_limit, tol_c, counters,
-                    (char *)workspace + base, n, st);
-    prof_mark(st, 3, true);
-    g_launches += 3;
-    cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? 0 : -(int)e;
-  }
   // inner-Jacobi kernel variant: 5 (default; fastest at n = 16384 in
   // tools/bench_inner.py), 4 (register-resident R), 3 (batched applies)
   static const int inner_variant = [] {
@@ -927,6 +917,42 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
     prof_mark(st, 2, true);
     g_launches += 3;
   }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : -(int)e;
+}
+
+// Diagnostic: record one {item, smid, start ns, end ns} int64 record per
+// cycle-engine work item into buf (device, int64[4 + 4 cap]; buf[0] = count)
+// on subsequent launches; buf = NULL disables.
+int jh_cycle_trace(void *buf, int64_t cap) {
+  cycle_trace(buf, cap);
+  return 0;
+}
+
+// jh_block_sweep on the cycle engine (jh_cycle.cu): the same p-steps,
+// bitwise the same results, in one persistent kernel.  plan = device copy of
+// jh_cycle_plan's output for this pivot table (NULL, another width, or
+// unaligned shapes fall back to jh_block_sweep).
+int jh_block_sweep_cycle(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int64_t ldv,
+                         int64_t nv, int w, const int32_t *outer, const int32_t *plan,
+                         int first_step, int nsteps, const int32_t *inner, int64_t n_plus,
+                         int inner_limit, double tol_c, void *workspace, int64_t ws_bytes,
+                         unsigned long long *counters, void *stream) {
+  static const bool force_simple = getenv("JHSVD_FORCE_SIMPLE") != nullptr;
+  const int b = (int)(n / (w > 1 ? w / 2 : 1));
+  if (!plan || force_simple || w % 2 || n % w || !cycle_ok(w, m, ldg, V ? nv : 0, V ? ldv : 0) ||
+      nsteps <= 0 || first_step < 0 || first_step + nsteps > b - 1)
+    return jh_block_sweep(G, ldg, m, n, V, ldv, nv, w, outer, first_step, nsteps, inner, n_plus,
+                          inner_limit, tol_c, workspace, ws_bytes, counters, stream);
+  if (ws_bytes < jh_sweep_workspace_bytes(n, w)) return -1001;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t ntask = n / w;
+  const int64_t base = ntask * (int64_t)w * w * 8 * 2 + ntask * 8 + 256;
+  prof_mark(st, 3, false);
+  launch_cycle(G, ldg, m, V, ldv, nv, outer, plan, b, first_step, nsteps, inner, n_plus,
+               inner_limit, tol_c, counters, (char *)workspace + base, st);
+  prof_mark(st, 3, true);
+  g_launches += 2;
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : -(int)e;
 }

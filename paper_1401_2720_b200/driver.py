@@ -104,7 +104,13 @@ class SweepEngine:
     pivot tables, task workspace and the per-sweep counters."""
 
     def __init__(self, m: int, n: int, nv: int, cfg: SolverConfig,
-                 outer: PStrategy, inner: PStrategy, n_plus: int):
+                 outer: PStrategy, inner: PStrategy, n_plus: int,
+                 cycle: Optional[bool] = None):
+        """``cycle``: run sweeps on the cycle engine when the outer table
+        allows it (default: the JHSVD_CYCLE=1 environment switch; it is
+        bitwise equal to the per-p-step kernels but not yet faster)."""
+        import os
+
         import torch
 
         self.lib = _lib.require_cuda()
@@ -121,11 +127,29 @@ class SweepEngine:
         self.outer_dev = torch.from_numpy(np.array(as_table(outer))).to(dev)
         self.inner_dev = torch.from_numpy(np.array(as_table(inner))).to(dev)
         self.nsteps = outer.num_steps
+        if cycle is None:
+            cycle = os.environ.get("JHSVD_CYCLE", "0") == "1"
+        self.plan_dev = self._cycle_plan(outer) if cycle else None
         nbytes = int(self.lib.jh_sweep_workspace_bytes(n, w))
         self.ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
         self.counters = torch.empty(4, dtype=torch.int64, device=dev)
         self.tasks_rotated: list[int] = []
         self.tol_c = EPS * math.sqrt(w) * cfg.eps_factor
+
+    def _cycle_plan(self, outer: PStrategy):
+        """Device copy of the cycle-engine plan of the outer table (None when
+        the table lacks the 4-cycle structure or the width is not 32)."""
+        import torch
+
+        b = outer.n
+        nints = int(self.lib.jh_cycle_plan_ints(b)) if self.w == 32 else 0
+        if nints <= 0:
+            return None
+        table = np.ascontiguousarray(np.array(as_table(outer), dtype=np.int32))
+        plan = np.empty(nints, dtype=np.int32)
+        if self.lib.jh_cycle_plan(table.ctypes.data, b, plan.ctypes.data) != 0:
+            return None
+        return torch.from_numpy(plan).to(_dev.device())
 
     def sweep(self, G, V, first_step: int = 0, nsteps: Optional[int] = None,
               n_plus: Optional[int] = None):
@@ -136,10 +160,12 @@ class SweepEngine:
         self.counters.zero_()
         self.counters[2].fill_(-1)
         ns = self.nsteps - first_step if nsteps is None else nsteps
-        rc = self.lib.jh_block_sweep(
+        rc = self.lib.jh_block_sweep_cycle(
             G.data_ptr(), self.m, self.m, self.n,
             V.data_ptr() if V is not None else None, self.nv, self.nv,
-            self.w, self.outer_dev.data_ptr(), int(first_step), int(ns),
+            self.w, self.outer_dev.data_ptr(),
+            self.plan_dev.data_ptr() if self.plan_dev is not None else None,
+            int(first_step), int(ns),
             self.inner_dev.data_ptr(), self.n_plus if n_plus is None else int(n_plus),
             self.cfg.inner_sweep_limit, self.tol_c,
             self.ws.data_ptr(), self.ws.numel(), self.counters.data_ptr(),

@@ -34,7 +34,48 @@ def main():
     return res
 
 
-if __name__ == "__main__" and "--latency" not in sys.argv:
+def timed(lib, kind, ctas, threads, iters, out):
+    for rep in range(2):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _lib.check(lib.jh_probe_rate(kind, ctas, threads, iters, out.data_ptr(),
+                                     _lib.stream_handle()), "rate")
+        e1.record()
+        torch.cuda.synchronize()
+    return e0.elapsed_time(e1)
+
+
+def chains_and_mixed():
+    """DMMA rate vs independent chains per warp (1 warp per SMSP, i.e. 4 per
+    SM, and 1 per SM), and DMMA + DFMA warps side by side."""
+    lib = _lib.require_cuda()
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    clk = torch.cuda.clock_rate() if hasattr(torch.cuda, "clock_rate") else None
+    iters = 20000
+    for wps in (1, 4, 8):
+        for c in (1, 2, 4, 8, 16):
+            kind = {1: 11, 2: 12, 4: 14, 8: 18, 16: 26}[c]
+            ctas, threads = sms * max(1, wps // 4), 32 * min(wps, 4)
+            ms = timed(lib, kind, ctas, threads, iters, out)
+            fma = ctas * threads / 32 * iters * 8 * 256
+            tf = 2 * fma / ms / 1e9
+            # cycles per dependent DMMA of one chain at the observed rate
+            ns_per = ms * 1e6 / (iters * 8 / c)
+            print(json.dumps({"probe": "dmma_chains", "warps_per_sm": wps, "chains": c,
+                              "tflops": tf, "ns_per_chain_step": ns_per}), flush=True)
+    for wps in (8, 16):
+        ctas, threads = sms * (wps // 8), 256
+        ms = timed(lib, 2, ctas, threads, iters, out)
+        fma = ctas * threads / 32 * iters * 8 * 256  # same per warp for both halves
+        print(json.dumps({"probe": "dmma+dfma", "warps_per_sm": wps,
+                          "tflops_combined": 2 * fma / ms / 1e9}), flush=True)
+
+
+if __name__ == "__main__" and "--chains" in sys.argv:
+    chains_and_mixed()
+elif __name__ == "__main__" and "--latency" not in sys.argv:
     main()
 
 

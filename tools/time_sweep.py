@@ -35,6 +35,13 @@ def main():
     from paper_1401_2720_b200 import _lib
 
     lib = _lib.load_library()
+    import os
+
+    trace = None
+    if os.environ.get("TRACE"):
+        cap = 4_000_000
+        trace = torch.zeros(4 + 4 * cap, dtype=torch.int64, device="cuda")
+        lib.jh_cycle_trace(trace.data_ptr(), cap)
     for s in range(sweeps):
         lib.jh_profile_begin(4 * eng.nsteps + 16)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -51,7 +58,7 @@ def main():
         print(f"n={n} w={w} sweep {s}: {ms:.1f} ms for {ns} p-steps "
               f"({ms / ns:.3f} ms/p-step) rot={rot} proper={proper} key={key} "
               f"rotated_tasks={nrot}", flush=True)
-        names = ("gram", "factor_inner", "update", "dataflow")
+        names = ("gram", "factor_inner", "update", "cycle")
         ntask = n // w
         for k in range(4):
             if pcnt[k] == 0:
@@ -69,6 +76,48 @@ def main():
                 byts = nst * ntask * 8.0 * w * n + nrot * 16.0 * w * 2 * n
                 extra = f" {byts / (pms[k] / 1e3) / 1e9:.0f} GB/s (Gram + update bytes)"
             print(f"   {names[k]:13s} {pms[k]:9.2f} ms total, {per * 1e3:9.1f} us/launch{extra}")
+        if trace is not None:
+            report_trace(trace, steps or eng.nsteps)
+            lib.jh_cycle_trace(None, 0)
+            trace = None
+
+
+def report_trace(trace, nsteps):
+    """Per item type: count, mean / max duration, busy share; and the
+    critical-path chain B -> I -> B per p-step."""
+    import numpy as np
+
+    cnt = int(trace[0].item())
+    rec = trace[4: 4 + 4 * cnt].view(cnt, 4).cpu().numpy()
+    rec = rec[((rec[:, 1] >> 16) & 0xFFFF) == 0]  # one record per cluster (rank 0)
+    item, smid, t0, t1 = rec[:, 0], rec[:, 1] & 0xFFFF, rec[:, 2], rec[:, 3]
+    stream_us = rec[:, 1] >> 32
+    cnt = len(rec)
+    typ = (item >> 60) & 0xF
+    a = (item >> 40) & 0xFFFFF
+    dur = (t1 - t0) / 1e3
+    tmin, tmax = t0.min(), t1.max()
+    span = (tmax - tmin) / 1e3
+    print(f"   trace: {cnt} items over {span:.0f} us on {len(np.unique(smid))} SMs (rank-0 CTAs)")
+    for k, name in enumerate(("B", "I", "V")):
+        m = typ == k
+        if m.any():
+            print(f"     {name}: n={m.sum():7d} mean {dur[m].mean():8.1f} us  p50 {np.median(dur[m]):8.1f}"
+                  f"  max {dur[m].max():8.1f}  busy {dur[m].sum() / span:6.1f} clusters avg"
+                  + (f"  (stream part mean {stream_us[m].mean():.1f} us)" if k == 0 else ""))
+    # per-boundary: first start and last end of B items, I items per step
+    for k, name in ((0, "B"),):
+        m = typ == k
+        st = a[m]
+        if k == 1:
+            st = st - st.min()
+        first = np.full(nsteps + 2, np.inf)
+        last = np.zeros(nsteps + 2)
+        np.minimum.at(first, st, (t0[m] - tmin) / 1e3)
+        np.maximum.at(last, st, (t1[m] - tmin) / 1e3)
+        sel = [0, 1, 2, nsteps // 2, nsteps - 1]
+        print(f"     {name} per step (first start / last end, us): " +
+              " ".join(f"[{i}] {first[i]:.0f}/{last[i]:.0f}" for i in sel if i <= nsteps))
 
 
 if __name__ == "__main__" and "--inner" not in sys.argv:
