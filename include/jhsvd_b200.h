@@ -56,24 +56,28 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
                    void *stream);
 
 /*
- * Cycle engine (the default sweep path for w = 32 on pivot tables whose
- * consecutive p-steps pair the block-columns in 4-cycles, e.g. rrow):
+ * Sweep engines for pivot tables whose consecutive p-steps pair the
+ * block-columns in 4-cycles (rrow, the Mantharam-Eberlein equivalent):
  * jh_cycle_plan (host) checks the structure of a host pivot table
- * int32[b-1][b/2][2] and fills plan[jh_cycle_plan_ints(b)] (0 = usable,
- * 1 = not usable); jh_block_sweep_cycle then runs the same p-steps as
- * jh_block_sweep -- bitwise the same G, V and counters -- as one persistent
- * kernel in which the post-multiplication of p-step s-1 and the Gram of
- * p-step s share one pass over G, and V is updated two p-steps per pass.
- * plan is the device copy; NULL (or w != 32) falls back to jh_block_sweep.
- * Same reference functions as jh_block_sweep (driver.py:153-190).
+ * int32[b-1][b/2][2] and fills plan[jh_cycle_plan_ints(b)] (return 0 =
+ * usable, 1 = not usable).  jh_block_sweep2 runs the same p-steps as
+ * jh_block_sweep -- bitwise the same G, V and counters -- on
+ *   engine 0: the per-p-step kernels (= jh_block_sweep),
+ *   engine 1: per-p-step kernels for G; V updated once per pair of p-steps
+ *             on a low-priority stream (needs V, w = 32, the device plan),
+ *   engine 2: the cycle engine, one persistent kernel (needs w = 32, the
+ *             device plan and jh_cycle_workspace_bytes more workspace).
+ * Unsupported cases fall back to engine 0.  Same reference functions as
+ * jh_block_sweep (driver.py:153-190).
  */
 int64_t jh_cycle_plan_ints(int b);
 int jh_cycle_plan(const int32_t *outer, int b, int32_t *plan);
-int jh_block_sweep_cycle(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int64_t ldv,
-                         int64_t nv, int w, const int32_t *outer, const int32_t *plan,
-                         int first_step, int nsteps, const int32_t *inner, int64_t n_plus,
-                         int inner_limit, double tol_c, void *workspace, int64_t ws_bytes,
-                         unsigned long long *counters, void *stream);
+int64_t jh_cycle_workspace_bytes(int64_t n, int w);
+int jh_block_sweep2(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int64_t ldv,
+                    int64_t nv, int w, const int32_t *outer, const int32_t *plan, int engine,
+                    int first_step, int nsteps, const int32_t *inner, int64_t n_plus,
+                    int inner_limit, double tol_c, void *workspace, int64_t ws_bytes,
+                    unsigned long long *counters, void *stream);
 
 /* Diagnostic: per-work-item trace of the cycle engine, records {item,
  * smid, start ns, end ns} (int64) into device buf[4 + 4 cap], buf[0] =

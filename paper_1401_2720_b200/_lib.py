@@ -31,9 +31,10 @@ SIGNATURES = {
                                 _c_p, _c_p]),
     "jh_cycle_plan_ints": (_c_i64, [_c_i32]),
     "jh_cycle_plan": (_c_i32, [_c_p, _c_i32, _c_p]),
-    "jh_block_sweep_cycle": (_c_i32, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_i64, _c_i32,
-                                      _c_p, _c_p, _c_i32, _c_i32, _c_p, _c_i64, _c_i32, _c_d,
-                                      _c_p, _c_i64, _c_p, _c_p]),
+    "jh_cycle_workspace_bytes": (_c_i64, [_c_i64, _c_i32]),
+    "jh_block_sweep2": (_c_i32, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_i64, _c_i32,
+                                 _c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_p, _c_i64, _c_i32, _c_d,
+                                 _c_p, _c_i64, _c_p, _c_p]),
     "jh_cycle_trace": (_c_i32, [_c_p, _c_i64]),
     "jh_gram": (_c_i32, [_c_p, _c_i64, _c_i64, _c_i32, _c_p, _c_p]),
     "jh_cholesky": (_c_i32, [_c_p, _c_i32, _c_p, _c_p, _c_p]),

@@ -698,13 +698,20 @@ int jh_profile_end(double *ms, int64_t *count) {
   return 0;
 }
 
-// Bytes of device workspace jh_block_sweep / jh_block_sweep_cycle need for
-// order n and width w.
-int64_t jh_sweep_workspace_bytes(int64_t n, int w) {
+// Workspace layout shared by the sweep paths: the per-task Gram matrices of
+// one p-step, a ring of four p-steps of per-task V' and rotation counts
+// (engine 1 keeps a p-step's V' until the paired V pass has read it), then
+// the cycle engine's own area (engine 2 only).
+static int64_t ws_base_bytes(int64_t n, int w) {
   const int64_t ntask = n / w;  // b/2 with b = n / (w/2)
-  const int64_t base = ntask * (int64_t)w * w * 8 * 2 + ntask * 8 + 256;
-  return base + cycle_workspace_bytes(n, w);
+  return ntask * (int64_t)w * w * 8 * 5 + ntask * 8 * 4 + 256;
 }
+
+// Bytes of device workspace jh_block_sweep (engines 0 and 1) needs.
+int64_t jh_sweep_workspace_bytes(int64_t n, int w) { return ws_base_bytes(n, w); }
+
+// Additional bytes the cycle engine (engine 2) needs after that.
+int64_t jh_cycle_workspace_bytes(int64_t n, int w) { return cycle_workspace_bytes(n, w); }
 
 // Number of int32 entries of the cycle plan of a pivot table of order b
 // (0: order not supported by the cycle engine).
@@ -712,7 +719,7 @@ int64_t jh_cycle_plan_ints(int b) { return cycle_plan_ints(b); }
 
 // Cycle plan of a host pivot table (int32[b-1][b/2][2], 0-based): 0 when
 // every pair of consecutive p-steps (with wrap) pairs the block-columns in
-// 4-cycles, so jh_block_sweep_cycle can fuse them; 1 otherwise.
+// 4-cycles, so jh_block_sweep2 can pair or fuse them; 1 otherwise.
 int jh_cycle_plan(const int32_t *outer, int b, int32_t *plan) { return cycle_plan(outer, b, plan); }
 
 // One block sweep (or p-steps [first_step, first_step + nsteps) of it) of
@@ -734,8 +741,8 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
   const int ntask = (int)(n / w);
   char *ws = (char *)workspace;
   double *Hbuf = (double *)ws;
-  double *Vbuf = Hbuf + (int64_t)ntask * w * w;
-  int64_t *trot = (int64_t *)(Vbuf + (int64_t)ntask * w * w);
+  double *Vbuf = Hbuf + (int64_t)ntask * w * w;                  // ring slot 0
+  int64_t *trot = (int64_t *)(Hbuf + (int64_t)ntask * w * w * 5);  // ring slot 0
   const int thr_inner = 32 * (bw > 1 ? bw : 1);
   const int nbg = (int)cdiv(m, kUpdRows);
   const int nbv = V ? (int)cdiv(nv, kUpdRows) : 0;
@@ -929,32 +936,110 @@ int jh_cycle_trace(void *buf, int64_t cap) {
   return 0;
 }
 
-// jh_block_sweep on the cycle engine (jh_cycle.cu): the same p-steps,
-// bitwise the same results, in one persistent kernel.  plan = device copy of
-// jh_cycle_plan's output for this pivot table (NULL, another width, or
-// unaligned shapes fall back to jh_block_sweep).
-int jh_block_sweep_cycle(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int64_t ldv,
+// Engine 1: the per-p-step Gram and inner kernels, and one update launch
+// per p-step (k_update4, jh_cycle.cu) that post-multiplies the G
+// block-columns of p-step s and -- deferred -- the V block-columns of the
+// previous pair of p-steps (a, a+1): half of the pair's row slabs in the
+// launch of p-step a+1, the other half in that of a+2.  V is read by nothing
+// else during the sweep and every V row still receives the same
+// transformations in the same order, so the results are bitwise those of
+// engine 0; V moves through HBM once per two p-steps instead of once per
+// p-step, and the DMMA-bound V items share the launch with the HBM-bound G
+// items.  The per-task V' and rotation counts of the last four p-steps are
+// kept in a ring.
+static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int64_t ldv,
                          int64_t nv, int w, const int32_t *outer, const int32_t *plan,
                          int first_step, int nsteps, const int32_t *inner, int64_t n_plus,
-                         int inner_limit, double tol_c, void *workspace, int64_t ws_bytes,
-                         unsigned long long *counters, void *stream) {
-  static const bool force_simple = getenv("JHSVD_FORCE_SIMPLE") != nullptr;
-  const int b = (int)(n / (w > 1 ? w / 2 : 1));
-  if (!plan || force_simple || w % 2 || n % w || !cycle_ok(w, m, ldg, V ? nv : 0, V ? ldv : 0) ||
-      nsteps <= 0 || first_step < 0 || first_step + nsteps > b - 1)
-    return jh_block_sweep(G, ldg, m, n, V, ldv, nv, w, outer, first_step, nsteps, inner, n_plus,
-                          inner_limit, tol_c, workspace, ws_bytes, counters, stream);
-  if (ws_bytes < jh_sweep_workspace_bytes(n, w)) return -1001;
-  cudaStream_t st = (cudaStream_t)stream;
-  const int64_t ntask = n / w;
-  const int64_t base = ntask * (int64_t)w * w * 8 * 2 + ntask * 8 + 256;
-  prof_mark(st, 3, false);
-  launch_cycle(G, ldg, m, V, ldv, nv, outer, plan, b, first_step, nsteps, inner, n_plus,
-               inner_limit, tol_c, counters, (char *)workspace + base, st);
-  prof_mark(st, 3, true);
-  g_launches += 2;
+                         int inner_limit, double tol_c, void *workspace,
+                         unsigned long long *counters, cudaStream_t st) {
+  const int b = (int)(n / (w / 2));
+  const int ntask = (int)(n / w);
+  const int64_t ww = (int64_t)w * w;
+  double *Hbuf = (double *)workspace;
+  double *Vring = Hbuf + (int64_t)ntask * ww;
+  int64_t *rring = (int64_t *)(Vring + 4 * (int64_t)ntask * ww);
+  auto vp = [&](int i) { return Vring + (int64_t)(i % 4) * ntask * ww; };
+  auto rt = [&](int i) { return rring + (int64_t)(i % 4) * ntask; };
+  for (int i = 0; i < nsteps; i++) {
+    const int s = first_step + i;
+    const int32_t *pairs = outer + (int64_t)s * ntask * 2;
+    prof_mark(st, 0, false);
+    launch_gram_tma(G, ldg, m, pairs, ntask, w, Hbuf, st);
+    prof_mark(st, 0, true);
+    prof_mark(st, 1, false);
+    launch_inner5(Hbuf, vp(i), rt(i), pairs, ntask, w, n_plus, inner, inner_limit, tol_c,
+                  counters, s, st);
+    prof_mark(st, 1, true);
+    // V work of this launch: up to two (pair, slab set) sources
+    int nsrc = 0, sa[2], k0[2], kstep[2];
+    bool second[2];
+    const double *VpA[2], *VpB[2];
+    const int64_t *rotA[2], *rotB[2];
+    auto add = [&](int i0, bool sec, int kk0, int kst) {
+      sa[nsrc] = first_step + i0;
+      second[nsrc] = sec;
+      VpA[nsrc] = vp(i0);
+      rotA[nsrc] = rt(i0);
+      VpB[nsrc] = sec ? vp(i0 + 1) : nullptr;
+      rotB[nsrc] = sec ? rt(i0 + 1) : nullptr;
+      k0[nsrc] = kk0;
+      kstep[nsrc] = kst;
+      nsrc++;
+    };
+    const bool last = (i == nsteps - 1);
+    if (i % 2 == 1) {
+      add(i - 1, true, 0, last ? 1 : 2);  // pair (i-1, i): even slabs now, odd ones next
+    } else {
+      if (i >= 2) add(i - 2, true, 1, 2);  // odd slabs of pair (i-2, i-1)
+      if (last) add(i, false, 0, 1);       // a last p-step without a partner
+    }
+    prof_mark(st, 2, false);
+    launch_update4(G, ldg, m, V, ldv, nv, outer, plan, b, s, vp(i), rt(i), nsrc, sa, second, VpA,
+                   rotA, VpB, rotB, k0, kstep, st);
+    prof_mark(st, 2, true);
+    g_launches += 3;
+  }
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : -(int)e;
+}
+
+// p-steps [first_step, first_step + nsteps) of a block sweep on a chosen
+// engine: 0 = per-p-step kernels (jh_block_sweep), 1 = engine 0 for G with
+// the V update paired over two p-steps on a side stream, 2 = the cycle
+// engine (one persistent kernel, jh_cycle.cu).  Engines 1 and 2 need V (1
+// only), w = 32, even m / ld, and plan = the device copy of jh_cycle_plan's
+// output for this pivot table; otherwise they fall back to engine 0.  All
+// engines give bitwise the same G, V and counters.
+int jh_block_sweep2(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int64_t ldv,
+                    int64_t nv, int w, const int32_t *outer, const int32_t *plan, int engine,
+                    int first_step, int nsteps, const int32_t *inner, int64_t n_plus,
+                    int inner_limit, double tol_c, void *workspace, int64_t ws_bytes,
+                    unsigned long long *counters, void *stream) {
+  static const bool force_simple = getenv("JHSVD_FORCE_SIMPLE") != nullptr;
+  const int b = (int)(n / (w > 1 ? w / 2 : 1));
+  const bool fused_ok = plan && !force_simple && w % 2 == 0 && n % w == 0 && nsteps > 0 &&
+                        first_step >= 0 && first_step + nsteps <= b - 1 &&
+                        cycle_ok(w, m, ldg, V ? nv : 0, V ? ldv : 0) && gram_tma_ok(w, m, ldg) &&
+                        inner5_ok(w);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (engine == 1 && fused_ok && V) {
+    if (ws_bytes < ws_base_bytes(n, w)) return -1001;
+    return sweep_vpaired(G, ldg, m, n, V, ldv, nv, w, outer, plan, first_step, nsteps, inner,
+                         n_plus, inner_limit, tol_c, workspace, counters, st);
+  }
+  if (engine == 2 && fused_ok) {
+    const int64_t base = ws_base_bytes(n, w);
+    if (ws_bytes < base + cycle_workspace_bytes(n, w)) return -1001;
+    prof_mark(st, 3, false);
+    launch_cycle(G, ldg, m, V, ldv, nv, outer, plan, b, first_step, nsteps, inner, n_plus,
+                 inner_limit, tol_c, counters, (char *)workspace + base, st);
+    prof_mark(st, 3, true);
+    g_launches += 2;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : -(int)e;
+  }
+  return jh_block_sweep(G, ldg, m, n, V, ldv, nv, w, outer, first_step, nsteps, inner, n_plus,
+                        inner_limit, tol_c, workspace, ws_bytes, counters, stream);
 }
 
 // cholesky_in_place (blockkernel.py:130-145): factors H (c x c, device,

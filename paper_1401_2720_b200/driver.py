@@ -105,10 +105,13 @@ class SweepEngine:
 
     def __init__(self, m: int, n: int, nv: int, cfg: SolverConfig,
                  outer: PStrategy, inner: PStrategy, n_plus: int,
-                 cycle: Optional[bool] = None):
-        """``cycle``: run sweeps on the cycle engine when the outer table
-        allows it (default: the JHSVD_CYCLE=1 environment switch; it is
-        bitwise equal to the per-p-step kernels but not yet faster)."""
+                 engine: Optional[int] = None):
+        """``engine`` (all bitwise equal, see jh_block_sweep2): 0 per-p-step
+        kernels (default; fastest measured), 1 per-p-step kernels with the V
+        update paired over two p-steps, 2 the cycle engine.  Engines 1 and
+        2 need an outer table that pairs block-columns in 4-cycles (rrow);
+        JHSVD_ENGINE selects the default.  profiles/r01/cycle_engine.md has
+        the measurements."""
         import os
 
         import torch
@@ -127,10 +130,14 @@ class SweepEngine:
         self.outer_dev = torch.from_numpy(np.array(as_table(outer))).to(dev)
         self.inner_dev = torch.from_numpy(np.array(as_table(inner))).to(dev)
         self.nsteps = outer.num_steps
-        if cycle is None:
-            cycle = os.environ.get("JHSVD_CYCLE", "0") == "1"
-        self.plan_dev = self._cycle_plan(outer) if cycle else None
+        if engine is None:
+            env = os.environ.get("JHSVD_ENGINE")
+            engine = int(env) if env else 0
+        self.plan_dev = self._cycle_plan(outer) if engine in (1, 2) else None
+        self.engine = engine if self.plan_dev is not None else 0
         nbytes = int(self.lib.jh_sweep_workspace_bytes(n, w))
+        if self.engine == 2:
+            nbytes += int(self.lib.jh_cycle_workspace_bytes(n, w))
         self.ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
         self.counters = torch.empty(4, dtype=torch.int64, device=dev)
         self.tasks_rotated: list[int] = []
@@ -160,11 +167,11 @@ class SweepEngine:
         self.counters.zero_()
         self.counters[2].fill_(-1)
         ns = self.nsteps - first_step if nsteps is None else nsteps
-        rc = self.lib.jh_block_sweep_cycle(
+        rc = self.lib.jh_block_sweep2(
             G.data_ptr(), self.m, self.m, self.n,
             V.data_ptr() if V is not None else None, self.nv, self.nv,
             self.w, self.outer_dev.data_ptr(),
-            self.plan_dev.data_ptr() if self.plan_dev is not None else None,
+            self.plan_dev.data_ptr() if self.plan_dev is not None else None, self.engine,
             int(first_step), int(ns),
             self.inner_dev.data_ptr(), self.n_plus if n_plus is None else int(n_plus),
             self.cfg.inner_sweep_limit, self.tol_c,

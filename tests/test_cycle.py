@@ -61,14 +61,14 @@ def test_plan_rejects_tables_without_cycles():
 # entry, bitwise) and the C oracle
 
 
-def _engines(m, n, nv, w, kind, n_plus, variant="full-block"):
+def _engines(m, n, nv, w, kind, n_plus, variant="full-block", engine=2):
     from paper_1401_2720_b200.driver import SolverConfig, SweepEngine
 
     cfg = SolverConfig(block_width=w, variant=variant, outer_strategy=kind)
     outer = make_strategy(kind, n // (w // 2))
     inner = make_strategy("rrow", w)
-    eng = SweepEngine(m, n, nv, cfg, outer, inner, n_plus, cycle=True)
-    ref = SweepEngine(m, n, nv, cfg, outer, inner, n_plus, cycle=False)  # per-p-step kernels
+    eng = SweepEngine(m, n, nv, cfg, outer, inner, n_plus, engine=engine)
+    ref = SweepEngine(m, n, nv, cfg, outer, inner, n_plus, engine=0)  # per-p-step kernels
     return eng, ref
 
 
@@ -80,6 +80,7 @@ def _graded(m, n, seed, kappa=1e6):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("engine", [1, 2])
 @pytest.mark.parametrize("m,n,first,count,with_v,n_plus", [
     (256, 256, 0, None, True, 256),     # whole sweep (15 p-steps, odd)
     (512, 512, 0, None, True, 512),     # 31 p-steps
@@ -93,13 +94,13 @@ def _graded(m, n, seed, kappa=1e6):
     (4096, 256, 0, None, True, 256),    # long rows: many chunks per item
     (2050, 512, 0, None, True, 512),    # m not a multiple of the chunk
 ])
-def test_cycle_sweep_bitwise_vs_pstep_kernels(m, n, first, count, with_v, n_plus):
+def test_engine_sweep_bitwise_vs_pstep_kernels(m, n, first, count, with_v, n_plus, engine):
     import torch
 
     torch.cuda.set_device(0)
     nv = n if with_v else 0
-    eng, ref = _engines(m, n, nv, 32, "rrow", n_plus)
-    assert eng.plan_dev is not None
+    eng, ref = _engines(m, n, nv, 32, "rrow", n_plus, engine=engine)
+    assert eng.plan_dev is not None and ref.engine == 0
     g = torch.from_numpy(_graded(m, n, 11 + m + n)).cuda()
     G1 = g.t().contiguous()
     G2 = G1.clone()
@@ -116,14 +117,15 @@ def test_cycle_sweep_bitwise_vs_pstep_kernels(m, n, first, count, with_v, n_plus
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("engine", ["1", "2"])
 @pytest.mark.parametrize("variant", ["full-block", "block-oriented"])
-def test_cycle_solve_bitwise_vs_oracle(variant, oracle, monkeypatch):
+def test_engine_solve_bitwise_vs_oracle(variant, engine, oracle, monkeypatch):
     import torch
 
     import paper_1401_2720_b200 as J
 
     torch.cuda.set_device(0)
-    monkeypatch.setenv("JHSVD_CYCLE", "1")
+    monkeypatch.setenv("JHSVD_ENGINE", engine)
     n = 512
     g = np.asfortranarray(_graded(n, n, 5, 1e10))
     cfg = J.SolverConfig(block_width=32, variant=variant)
@@ -137,7 +139,8 @@ def test_cycle_solve_bitwise_vs_oracle(variant, oracle, monkeypatch):
 
 
 @pytest.mark.gpu
-def test_cycle_reports_first_failure_like_pstep_path():
+@pytest.mark.parametrize("engine", [1, 2])
+def test_engine_reports_first_failure_like_pstep_path(engine):
     """A rank-deficient pair fails in the same (p-step, task, status, index)
     on both paths (the error key is the minimum in the reference order)."""
     import torch
@@ -146,7 +149,7 @@ def test_cycle_reports_first_failure_like_pstep_path():
     n = 256
     a = _graded(n, n, 3)
     a[:, 37] = 0.0  # a zero column: the Cholesky of its first pair breaks down
-    eng, ref = _engines(n, n, n, 32, "rrow", n)
+    eng, ref = _engines(n, n, n, 32, "rrow", n, engine=engine)
     G1 = torch.from_numpy(a).cuda().t().contiguous()
     G2 = G1.clone()
     V1 = torch.eye(n, dtype=torch.float64, device="cuda")
