@@ -68,16 +68,18 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
  *   engine 2: the cycle engine, one persistent kernel (needs w = 32, the
  *             device plan and jh_cycle_workspace_bytes more workspace).
  * Unsupported cases fall back to engine 0.  Same reference functions as
- * jh_block_sweep (driver.py:153-190).
+ * jh_block_sweep (driver.py:153-190).  shortening: 0 = Gram + Cholesky
+ * (blockkernel.py:76-145), 1 = QR peel-off (blockkernel.py:148-244; per
+ * p-step kernels, w in {16, 32}, m % w == 0; -1000 otherwise).
  */
 int64_t jh_cycle_plan_ints(int b);
 int jh_cycle_plan(const int32_t *outer, int b, int32_t *plan);
 int64_t jh_cycle_workspace_bytes(int64_t n, int w);
 int jh_block_sweep2(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int64_t ldv,
                     int64_t nv, int w, const int32_t *outer, const int32_t *plan, int engine,
-                    int first_step, int nsteps, const int32_t *inner, int64_t n_plus,
-                    int inner_limit, double tol_c, void *workspace, int64_t ws_bytes,
-                    unsigned long long *counters, void *stream);
+                    int shortening, int first_step, int nsteps, const int32_t *inner,
+                    int64_t n_plus, int inner_limit, double tol_c, void *workspace,
+                    int64_t ws_bytes, unsigned long long *counters, void *stream);
 
 /* Diagnostic: per-work-item trace of the cycle engine, records {item,
  * smid, start ns, end ns} (int64) into device buf[4 + 4 cap], buf[0] =
@@ -90,6 +92,10 @@ int jh_gram(const double *A, int64_t lda, int64_t m, int c, double *H, void *str
 /* cholesky_in_place (blockkernel.py:130-145): H (c x c) overwritten with L,
  * R = L^T; *info (device int) = 0 or the 1-based bad pivot. */
 int jh_cholesky(double *H, int c, double *R, int *info, void *stream);
+
+/* qr_peeloff (blockkernel.py:223-244): R (c x c, column-major, nonnegative
+ * diagonal) of A (m x c), c even <= 32, m a positive multiple of c. */
+int jh_qr_peeloff(const double *A, int64_t lda, int64_t m, int c, double *R, void *stream);
 
 /* inner_jacobi (blockkernel.py:346-400) on one c x c factor, c even <= 64.
  * R in place, V = accumulated transformation; out (device int64[5]) =

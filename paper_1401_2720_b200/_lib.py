@@ -33,10 +33,11 @@ SIGNATURES = {
     "jh_cycle_plan": (_c_i32, [_c_p, _c_i32, _c_p]),
     "jh_cycle_workspace_bytes": (_c_i64, [_c_i64, _c_i32]),
     "jh_block_sweep2": (_c_i32, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_i64, _c_i32,
-                                 _c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_p, _c_i64, _c_i32, _c_d,
-                                 _c_p, _c_i64, _c_p, _c_p]),
+                                 _c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_i64,
+                                 _c_i32, _c_d, _c_p, _c_i64, _c_p, _c_p]),
     "jh_cycle_trace": (_c_i32, [_c_p, _c_i64]),
     "jh_gram": (_c_i32, [_c_p, _c_i64, _c_i64, _c_i32, _c_p, _c_p]),
+    "jh_qr_peeloff": (_c_i32, [_c_p, _c_i64, _c_i64, _c_i32, _c_p, _c_p]),
     "jh_cholesky": (_c_i32, [_c_p, _c_i32, _c_p, _c_p, _c_p]),
     "jh_inner_jacobi": (_c_i32, [_c_p, _c_p, _c_i32, _c_p, _c_p, _c_d, _c_i32, _c_p, _c_p]),
     "jh_gemm": (_c_i32, [_c_p, _c_i64, _c_i64, _c_i32, _c_p, _c_i64, _c_i32, _c_p, _c_i64, _c_p]),

@@ -12,12 +12,13 @@ __global__ void __launch_bounds__(InnerCfg5<W>::NTH)
 k_factor_inner5(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
                 int64_t *__restrict__ task_rot, const int32_t *__restrict__ pairs,
                 int64_t n_plus, const int32_t *__restrict__ inner, int inner_limit,
-                double tol_c, unsigned long long *counters, int pstep) {
+                double tol_c, unsigned long long *counters, int pstep, bool from_r) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int task = blockIdx.x;
   inner5_task<W, InnerCfg5<W>::NTH>(smraw, Hbuf + (size_t)task * W * W, Vbuf + (size_t)task * W * W,
                                     pairs[2 * task], pairs[2 * task + 1], n_plus, inner,
-                                    inner_limit, tol_c, counters, pstep, task, &task_rot[task]);
+                                    inner_limit, tol_c, counters, pstep, task, &task_rot[task],
+                                    from_r);
 }
 
 bool inner5_ok(int w) { return w == 16 || w == 32 || w == 64; }
@@ -26,7 +27,7 @@ template <int W>
 static void launch_inner5_t(const double *Hbuf, double *Vbuf, int64_t *trot, const int32_t *pairs,
                            int ntask, int64_t n_plus, const int32_t *inner, int inner_limit,
                            double tol_c, unsigned long long *counters, int pstep,
-                           cudaStream_t st) {
+                           cudaStream_t st, bool from_r) {
   const size_t smem = sizeof(InnerSmem5<W>);
   static bool attr = false;
   if (!attr) {
@@ -35,21 +36,23 @@ static void launch_inner5_t(const double *Hbuf, double *Vbuf, int64_t *trot, con
     attr = true;
   }
   k_factor_inner5<W><<<ntask, InnerCfg5<W>::NTH, smem, st>>>(Hbuf, Vbuf, trot, pairs, n_plus, inner,
-                                                           inner_limit, tol_c, counters, pstep);
+                                                           inner_limit, tol_c, counters, pstep,
+                                                           from_r);
 }
 
 void launch_inner5(const double *Hbuf, double *Vbuf, int64_t *trot, const int32_t *pairs,
                    int ntask, int w, int64_t n_plus, const int32_t *inner, int inner_limit,
-                   double tol_c, unsigned long long *counters, int pstep, cudaStream_t st) {
+                   double tol_c, unsigned long long *counters, int pstep, cudaStream_t st,
+                   bool from_r) {
   if (w == 16)
     launch_inner5_t<16>(Hbuf, Vbuf, trot, pairs, ntask, n_plus, inner, inner_limit, tol_c,
-                       counters, pstep, st);
+                       counters, pstep, st, from_r);
   else if (w == 32)
     launch_inner5_t<32>(Hbuf, Vbuf, trot, pairs, ntask, n_plus, inner, inner_limit, tol_c,
-                       counters, pstep, st);
+                       counters, pstep, st, from_r);
   else
     launch_inner5_t<64>(Hbuf, Vbuf, trot, pairs, ntask, n_plus, inner, inner_limit, tol_c,
-                       counters, pstep, st);
+                       counters, pstep, st, from_r);
 }
 
 }  // namespace jh

@@ -63,7 +63,8 @@ __device__ __noinline__ long long inner5_task(unsigned char *smem, const double 
                                               int64_t n_plus, const int32_t *__restrict__ inner,
                                               int inner_limit, double tol_c,
                                               unsigned long long *counters, int pstep,
-                                              int task_key, int64_t *rot_out) {
+                                              int task_key, int64_t *rot_out,
+                                              bool from_r = false) {
   constexpr int HALF = InnerCfg5<W>::HALF, LD = InnerCfg5<W>::LD;
   constexpr int BW = W / 2, NSTEP = W - 1;
   InnerSmem5<W> &S = *reinterpret_cast<InnerSmem5<W> *>(smem);
@@ -85,6 +86,15 @@ __device__ __noinline__ long long inner5_task(unsigned char *smem, const double 
     S.stop = 0;
   }
   __syncthreads();
+  if (from_r) {
+    // Hg already holds the shortened factor R (QR peel-off, column-major,
+    // zero strict lower triangle): no Cholesky
+    for (int e = tid; e < W * W; e += NTH) {
+      const int j = e / W, i = e - j * W;
+      S.R[j * LD + i] = S.H[e];
+    }
+    __syncthreads();
+  } else {
 
   // ---- forward-looking Cholesky (reference element order), lower triangle
   {
@@ -121,6 +131,7 @@ __device__ __noinline__ long long inner5_task(unsigned char *smem, const double 
     S.R[j * LD + i] = (i <= j) ? S.H[i * W + j] : 0.0;
   }
   __syncthreads();
+  }  // !from_r
 
   // ---- inner sweeps
   int a_r = 0, b_r = 0;  // lane-private counters of warp 0

@@ -40,9 +40,17 @@ void launch_fused(double *G, int64_t ldg, int64_t m, double *V, int64_t ldv, int
 
 // the first v3 inner Jacobi, kept for A/B timing (jh_inner5.cu)
 bool inner5_ok(int w);
+// from_r: Hbuf holds the shortened factors R (QR peel-off) instead of Grams
 void launch_inner5(const double *Hbuf, double *Vbuf, int64_t *trot, const int32_t *pairs,
                    int ntask, int w, int64_t n_plus, const int32_t *inner, int inner_limit,
-                   double tol_c, unsigned long long *counters, int pstep, cudaStream_t st);
+                   double tol_c, unsigned long long *counters, int pstep, cudaStream_t st,
+                   bool from_r = false);
+
+// QR peel-off shortening of every task of a p-step (jh_qr.cu): Rbuf[task] =
+// R (w x w, column-major) of the pair [Gp Gq]; w even <= 32, m % w == 0
+bool qr_ok(int w, int64_t m);
+void launch_qr_peeloff(const double *G, int64_t ldg, int64_t m, const int32_t *pairs, int ntask,
+                       int w, double *Rbuf, cudaStream_t st);
 
 // cycle engine (jh_cycle.cu): p-steps [s_begin, s_begin + nsteps) of one
 // sweep in one persistent kernel, w = 32, pivot tables with the 4-cycle

@@ -1003,6 +1003,39 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
   return e == cudaSuccess ? 0 : -(int)e;
 }
 
+// QR peel-off shortening (shortening = 1, reference blockkernel.py:223-244):
+// per p-step the R factors of every task (jh_qr.cu), the inner Jacobi on R
+// (no Gram, no Cholesky), and the same post-multiplication.
+static int sweep_qr(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int64_t ldv,
+                    int64_t nv, int w, const int32_t *outer, int first_step, int nsteps,
+                    const int32_t *inner, int64_t n_plus, int inner_limit, double tol_c,
+                    void *workspace, int64_t ws_bytes, unsigned long long *counters,
+                    cudaStream_t st) {
+  if (w < 2 || w % 2 || n % w || !qr_ok(w, m)) return -1000;
+  if (ws_bytes < ws_base_bytes(n, w)) return -1001;
+  const int ntask = (int)(n / w);
+  const int64_t ww = (int64_t)w * w;
+  double *Rbuf = (double *)workspace;
+  double *Vbuf = Rbuf + (int64_t)ntask * ww;
+  int64_t *trot = (int64_t *)(Rbuf + (int64_t)ntask * ww * 5);
+  for (int s = first_step; s < first_step + nsteps; s++) {
+    const int32_t *pairs = outer + (int64_t)s * ntask * 2;
+    prof_mark(st, 0, false);
+    launch_qr_peeloff(G, ldg, m, pairs, ntask, w, Rbuf, st);
+    prof_mark(st, 0, true);
+    prof_mark(st, 1, false);
+    launch_inner5(Rbuf, Vbuf, trot, pairs, ntask, w, n_plus, inner, inner_limit, tol_c, counters,
+                  s, st, true);
+    prof_mark(st, 1, true);
+    prof_mark(st, 2, false);
+    launch_update_dmma(G, ldg, m, V, ldv, nv, pairs, ntask, w, Vbuf, trot, st);
+    prof_mark(st, 2, true);
+    g_launches += 3;
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : -(int)e;
+}
+
 // p-steps [first_step, first_step + nsteps) of a block sweep on a chosen
 // engine: 0 = per-p-step kernels (jh_block_sweep), 1 = engine 0 for G with
 // the V update paired over two p-steps on a side stream, 2 = the cycle
@@ -1012,10 +1045,14 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
 // engines give bitwise the same G, V and counters.
 int jh_block_sweep2(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int64_t ldv,
                     int64_t nv, int w, const int32_t *outer, const int32_t *plan, int engine,
-                    int first_step, int nsteps, const int32_t *inner, int64_t n_plus,
-                    int inner_limit, double tol_c, void *workspace, int64_t ws_bytes,
-                    unsigned long long *counters, void *stream) {
+                    int shortening, int first_step, int nsteps, const int32_t *inner,
+                    int64_t n_plus, int inner_limit, double tol_c, void *workspace,
+                    int64_t ws_bytes, unsigned long long *counters, void *stream) {
   static const bool force_simple = getenv("JHSVD_FORCE_SIMPLE") != nullptr;
+  if (shortening == 1)
+    return sweep_qr(G, ldg, m, n, V, ldv, nv, w, outer, first_step, nsteps, inner, n_plus,
+                    inner_limit, tol_c, workspace, ws_bytes, counters, (cudaStream_t)stream);
+  if (shortening != 0) return -1000;
   const int b = (int)(n / (w > 1 ? w / 2 : 1));
   const bool fused_ok = plan && !force_simple && w % 2 == 0 && n % w == 0 && nsteps > 0 &&
                         first_step >= 0 && first_step + nsteps <= b - 1 &&

@@ -121,8 +121,11 @@ class SweepEngine:
         w = cfg.block_width
         if w > MAX_GPU_BLOCK_WIDTH:
             raise ValueError(f"block_width {w} > {MAX_GPU_BLOCK_WIDTH} is not supported on the GPU")
-        if cfg.shortening != "cholesky":
-            raise NotImplementedError("QR peel-off shortening is not implemented on the GPU yet")
+        if cfg.shortening == "qr" and (w not in (16, 32) or m % w):
+            raise NotImplementedError(
+                "QR peel-off shortening runs on the GPU for block widths 16 and 32 with "
+                "m a multiple of the width")
+        self.shortening = 1 if cfg.shortening == "qr" else 0
         self.m, self.n, self.nv, self.w = m, n, nv, w
         self.cfg = cfg
         self.outer = outer
@@ -172,7 +175,7 @@ class SweepEngine:
             V.data_ptr() if V is not None else None, self.nv, self.nv,
             self.w, self.outer_dev.data_ptr(),
             self.plan_dev.data_ptr() if self.plan_dev is not None else None, self.engine,
-            int(first_step), int(ns),
+            self.shortening, int(first_step), int(ns),
             self.inner_dev.data_ptr(), self.n_plus if n_plus is None else int(n_plus),
             self.cfg.inner_sweep_limit, self.tol_c,
             self.ws.data_ptr(), self.ws.numel(), self.counters.data_ptr(),

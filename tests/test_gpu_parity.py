@@ -52,6 +52,29 @@ def test_inner_jacobi_bitwise(kernels_golden):
         assert np.array_equal(res.v_acc, K[f"inner{k}_vacc"]), k
 
 
+def test_qr_peeloff_bitwise(kernels_golden):
+    K = kernels_golden
+    for k in range(3):
+        assert np.array_equal(J.qr_peeloff(K[f"qr{k}_in"]), K[f"qr{k}_out"]), k
+
+
+@pytest.mark.parametrize("n,w,kappa", [(512, 32, 1e8), (256, 16, 1e12)])
+def test_qr_shortening_bitwise_vs_oracle(n, w, kappa, oracle):
+    """The QR peel-off sweep path (SolverConfig.shortening = 'qr') against
+    the C oracle on a graded factor, bitwise."""
+    rng = np.random.default_rng(n + 7)
+    b = rng.standard_normal((n, n))
+    g = np.asfortranarray(b / np.linalg.norm(b, axis=0) * np.logspace(0, -np.log10(kappa), n))
+    cfg = J.SolverConfig(block_width=w, shortening="qr")
+    res = J.block_jacobi(g, None, cfg)
+    outer = S.as_table(S.make_strategy("rrow", n // (w // 2)))
+    inner = S.as_table(S.make_strategy("rrow", w))
+    ref = oracle.block_jacobi(g, n, cfg, outer, inner)
+    assert res.stats == ref.stats
+    assert np.array_equal(res.sigma, ref.sigma)
+    assert np.array_equal(res.u, ref.u) and np.array_equal(res.v, ref.v)
+
+
 def test_extract_sigma_bitwise(kernels_golden, oracle):
     K = kernels_golden
     for k in (0, 1, 2, 3, 4, 6):
@@ -62,7 +85,7 @@ def test_extract_sigma_bitwise(kernels_golden, oracle):
 
 
 SOLVES = ["config1", "diag4", "graded256_bo", "hsvd96", "n64_cap1", "n64_eps4", "n64_inner2",
-          "n64_nov", "n64_w16_bl", "n64_w16_col", "n64_w16_rcol", "n64_w16_row", "n64_w16_rrow",
+          "n64_nov", "n64_qr", "n64_w16_bl", "n64_w16_col", "n64_w16_rcol", "n64_w16_row", "n64_w16_rrow",
           "n64_w2_rrow", "n64_w4_rrow", "n64_w64_rrow", "n64_w8_mm", "n64_solvev",
           "type1_bo", "type1_fb", "type2_bo", "type2_fb", "type3_bo", "type3_fb", "type4_bo",
           "type4_fb"]
