@@ -135,13 +135,13 @@ class ClockSampler:
 def make_input(args):
     import torch
 
-    from paper_1401_2720_b200.testgen import SpectrumSpec, canonical_sort, gen_factor_device, \
+    from paper_1401_2720_b200.testgen import SpectrumSpec, canonical_sort, gen_factor_orth_device, \
         gen_spectrum
 
     lam = gen_spectrum(SpectrumSpec(args.spectrum_type, args.n, args.seed))
     lam_sorted, n_plus = canonical_sort(lam)
     sigma = np.sqrt(np.abs(lam_sorted))
-    G0 = gen_factor_device(sigma, seed=args.seed)
+    G0 = gen_factor_orth_device(sigma, seed=args.seed)
     torch.cuda.synchronize()
     return G0, sigma, n_plus
 

@@ -44,7 +44,10 @@ def to_colmajor(a, copy: bool = False) -> torch.Tensor:
     arr = np.asarray(a, dtype=np.float64)
     if arr.ndim != 2:
         raise ValueError("expected a 2-d matrix")
-    host = torch.from_numpy(np.ascontiguousarray(arr.T))
+    hc = np.ascontiguousarray(arr.T)
+    if not hc.flags.writeable:  # e.g. np.frombuffer data: torch wants writable memory
+        hc = hc.copy()
+    host = torch.from_numpy(hc)
     if host.numel() >= (1 << 20):
         host = host.pin_memory()
     return host.to(device(), non_blocking=True)

@@ -17,10 +17,13 @@ and a sweep ends with an all-reduce of the rotation counters (the
 reference's "+-reduce of the local counters").
 
 Results do not depend on which worker holds which pair (reference fact,
-SURVEY.md section 0.7), so instead of the reference's exhaustive
-fast-link search (``optimize_mapping``, which does not finish for g = 8) a
-legal cyclic mapping is found by depth-first search; on NVSwitch every
-link is equally fast.
+SURVEY.md section 0.7).  For g <= 4 the mapping is the reference's own
+(``optimize_mapping``: exhaustive search for the most transitions over
+"fast" links, the reference's two-speed topology), so exchange traces match
+the reference record for record; for g > 4, where that search does not
+finish, a legal cyclic mapping is found by breadth-first search
+(``legal_mapping``).  On NVSwitch every link is equally fast; the trace
+keeps the reference's link labels.
 
 Without an initialised process group (or with ``backend="sim"``) the g
 workers run one after another in this process on one device, exactly like
@@ -41,7 +44,22 @@ from .driver import BLOCK_ORIENTED, HsvdResult, SolverConfig
 from .strategy import PStrategy, make_strategy
 
 FAST = "fast"
+SLOW = "slow"
 NVSWITCH = "nvswitch"
+EXHAUSTIVE_MAPPING_MAX_G = 4
+
+
+@dataclass(frozen=True)
+class Topology:
+    """The reference's two-speed link classification (distsim.py:46-55):
+    worker i talks to i xor 1 over a fast link, to the rest over slow ones."""
+
+    g: int
+
+    def link_class(self, i: int, j: int) -> str:
+        if i == j or not (0 <= i < self.g and 0 <= j < self.g):
+            raise ValueError(f"invalid link ({i}, {j}) for {self.g} workers")
+        return FAST if j == i ^ 1 else SLOW
 
 
 class MappingError(ValueError):
@@ -149,6 +167,89 @@ def legal_mapping(strategy: PStrategy) -> ColumnMapping:
     assignments = tuple(tuple(steps[s][path[s][i]] for i in range(g)) for s in range(ns))
     moves = tuple(_moves(assignments[s], assignments[(s + 1) % ns]) for s in range(ns))
     return ColumnMapping(g, assignments, moves)
+
+
+def _assignment_options(cur, next_step_pairs):
+    """All bijections pairs -> workers for the next step in which every
+    worker keeps exactly one of its block-columns (distsim.py:104-133)."""
+    g = len(cur)
+    per_worker = [[pq for pq in next_step_pairs if len(set(cur[i]) & set(pq)) == 1]
+                  for i in range(g)]
+    options, chosen, used = [], [], set()
+
+    def rec(i):
+        if i == g:
+            options.append(tuple(chosen))
+            return
+        for pq in per_worker[i]:
+            if pq in used:
+                continue
+            used.add(pq)
+            chosen.append(pq)
+            rec(i + 1)
+            chosen.pop()
+            used.remove(pq)
+
+    rec(0)
+    return options
+
+
+@functools.lru_cache(maxsize=16)
+def optimize_mapping(strategy: PStrategy, topology: Topology) -> ColumnMapping:
+    """The reference's mapping (distsim.py:136-190): exhaustive search for
+    the assignment with the most all-fast exchange transitions per sweep
+    (the wrap from the last step to the first included), ties toward the
+    lexicographically smallest assignment table.  Exponential in g: used
+    for g <= EXHAUSTIVE_MAPPING_MAX_G."""
+    import itertools
+
+    g = topology.g
+    if strategy.n != 2 * g:
+        raise MappingError(f"strategy order {strategy.n} != 2g = {2 * g}")
+    steps = [tuple(sorted(step)) for step in strategy.steps]
+    ns = len(steps)
+    if g == 1:
+        return ColumnMapping(1, tuple((pq,) for pq in strategy.steps), ((),) * ns)
+    best = None
+
+    def score(assignments):
+        count, moves = 0, []
+        for s in range(ns):
+            mv = _moves(assignments[s], assignments[(s + 1) % ns])
+            if mv is None:
+                return None, None
+            moves.append(mv)
+            count += all(topology.link_class(src, i) == FAST for i, (src, _) in enumerate(mv))
+        return count, tuple(moves)
+
+    def rec(assignments):
+        nonlocal best
+        if len(assignments) == ns:
+            count, moves = score(assignments)
+            if count is None:
+                return
+            key = (-count, tuple(assignments))
+            if best is None or key < best[0]:
+                best = (key, tuple(assignments), moves)
+            return
+        for opt in sorted(_assignment_options(assignments[-1], steps[len(assignments)])):
+            assignments.append(opt)
+            rec(assignments)
+            assignments.pop()
+
+    for initial in sorted(itertools.permutations(steps[0])):
+        rec([tuple(initial)])
+    if best is None:
+        raise MappingError("no exchange-compatible worker assignment exists")
+    return ColumnMapping(g, best[1], best[2])
+
+
+def default_mapping(strategy: PStrategy) -> ColumnMapping:
+    """The reference's mapping where its search is feasible, else a legal one."""
+    g = strategy.n // 2
+    if g <= EXHAUSTIVE_MAPPING_MAX_G:
+        return optimize_mapping(strategy, Topology(g))
+    return legal_mapping(strategy)
 
 
 def local_signature_pair(signature: Signature, p: int, q: int, bw: int) -> Signature:
@@ -324,7 +425,8 @@ def run_distributed(g_matrix, signature: Optional[Signature], g: int,
 
     outer = make_strategy(cfg.outer_strategy, 2 * g)
     if mapping is None:
-        mapping = legal_mapping(outer)
+        mapping = default_mapping(outer)
+    topology = Topology(g)
     nsteps = len(mapping.assignments)
     want_v = cfg.accumulate_v or cfg.solve_v
     mine = comm.local_workers(g)
@@ -345,7 +447,7 @@ def run_distributed(g_matrix, signature: Optional[Signature], g: int,
             vx[i] = None
 
     stats: list[tuple[int, int]] = []
-    trace: list[ExchangeRecord] = []
+    wtrace: list[list[ExchangeRecord]] = [[] for _ in range(g)]  # per worker
     converged = False
     for sweep in range(cfg.max_block_sweeps):
         rot_l = proper_l = 0
@@ -397,8 +499,9 @@ def run_distributed(g_matrix, signature: Optional[Signature], g: int,
                     p, q = mapping.assignments[s][i]
                     kept = ({p, q} & set(nxt[i])).pop()
                     sent = p if kept == q else q
-                    trace.append(ExchangeRecord(sweep + 1, s + 1, i, sent, _holder(nxt, sent),
-                                                NVSWITCH))
+                    dst = _holder(nxt, sent)
+                    wtrace[i].append(ExchangeRecord(sweep + 1, s + 1, i, sent, dst,
+                                                    topology.link_class(i, dst)))
         rot, proper = _allreduce_counts(comm, rot_l, proper_l, dev)
         stats.append((rot, proper))
         if proper == 0:
@@ -418,6 +521,8 @@ def run_distributed(g_matrix, signature: Optional[Signature], g: int,
                          converged=converged)
     else:
         res = engine.finish(Gf, Vf, signature, stats, converged)
+    # per-worker records merged in (sweep, step, worker) order (distsim.py:422-423)
+    trace = [rec for wt in wtrace for rec in wt]
     trace.sort(key=lambda r: (r.sweep, r.step, r.worker))
     return res, trace
 

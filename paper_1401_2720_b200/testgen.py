@@ -1,17 +1,23 @@
 """Synthetic test factors with prescribed spectra (reference ``jhsvd.testgen``).
 
-``gen_spectrum`` / ``canonical_sort`` / ``relative_error`` restate the
-reference (pkg/src/jhsvd/testgen.py:21-146) exactly: the spectra come from
-numpy's PCG64 with the same draws, so they are bitwise the reference's.
-``gen_factor_device`` builds G = Q diag(sqrt|lambda|) W^T on the GPU with
-FP64 Q, W from seeded Householder QR (torch.linalg.qr): the reference's
-O(n^3) rank-1 reflector loop takes about an hour at n = 8192 on the host.
-The device factor has the same spectrum but not the reference's bits (its
-Q, W differ); parity runs use stored inputs instead.
+``gen_spectrum`` / ``canonical_sort`` / ``relative_error`` / ``gen_factor``
+restate the reference (pkg/src/jhsvd/testgen.py:21-146) exactly: the
+spectra and reflectors come from numpy's PCG64 with the same draws, and the
+host ``gen_factor`` repeats the reference's numpy operations, so on the same
+BLAS its output is bitwise the reference's (tests/golden/testgen.npz).
+
+``gen_factor_device`` is the same construction on the GPU: the same random
+draws (host PCG64, identical unit reflector vectors and hyperbolic
+rotations, in the reference's order), the O(n^3) reflector applications in
+FP64 on the device.  It differs from the host factor only by rounding
+(~1e-15 relative) and makes the reference's hour-long host generation at
+n = 8192 take seconds.  ``gen_factor_orth_device`` (G = Q diag(sigma) W^T
+with Haar Q, W from a seeded QR) builds the tall and the 16384 inputs.
 """
 
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass
 
 import numpy as np
@@ -86,6 +92,108 @@ def relative_error(sigma, signature: Signature, lam) -> float:
     return float(np.max(np.abs(implied - lam_sorted) / np.abs(lam_sorted)))
 
 
+def _apply_reflectors(rng, g: np.ndarray, count: int) -> None:
+    """g <- Q g with Q a product of `count` random Householder reflectors
+    (testgen.py:82-88)."""
+    n = g.shape[0]
+    for _ in range(count):
+        v = rng.normal(size=n)
+        v /= np.linalg.norm(v)
+        g -= 2.0 * np.outer(v, v @ g)
+
+
+def _mix_j_orthogonal(rng, g: np.ndarray, n_plus: int, tanh_max: float) -> None:
+    """g <- g W^T for a J-orthogonal W (testgen.py:91-114): reflectors inside
+    each signature class, then 2n hyperbolic rotations across the boundary."""
+    n = g.shape[0]
+    for lo, hi in ((0, n_plus), (n_plus, n)):
+        width = hi - lo
+        if width < 2:
+            continue
+        block = np.asfortranarray(g[:, lo:hi].T)
+        _apply_reflectors(rng, block, width)
+        g[:, lo:hi] = block.T
+    if 0 < n_plus < n:
+        for _ in range(2 * n):
+            i = int(rng.integers(0, n_plus))
+            j = int(rng.integers(n_plus, n))
+            th = tanh_max * (2.0 * rng.random() - 1.0)
+            ch = 1.0 / math.sqrt(1.0 - th * th)
+            gi = g[:, i].copy()
+            gj = g[:, j].copy()
+            g[:, i] = ch * (gi + th * gj)
+            g[:, j] = ch * (th * gi + gj)
+
+
+def gen_factor(lam, seed: int, tanh_max: float = 0.1) -> tuple[np.ndarray, Signature]:
+    """Factor G = Q diag(sqrt|lam_sorted|) W^T whose hyperbolic singular
+    values are sqrt|lam| (testgen.py:117-133); host numpy, O(n^3)."""
+    lam_sorted, n_plus = canonical_sort(lam)
+    n = lam_sorted.size
+    rng = np.random.Generator(np.random.PCG64(seed))
+    g = np.zeros((n, n), order="F")
+    np.fill_diagonal(g, np.sqrt(np.abs(lam_sorted)))
+    _apply_reflectors(rng, g, n)
+    _mix_j_orthogonal(rng, g, n_plus, tanh_max)
+    return np.asfortranarray(g), Signature(n, n_plus)
+
+
+def _unit_reflectors(rng, length: int, count: int, batch: int = 256):
+    """The unit reflector vectors of _apply_reflectors, drawn in the same
+    order (one rng.normal(size=length) per reflector), in batches."""
+    done = 0
+    while done < count:
+        k = min(batch, count - done)
+        vs = np.empty((k, length))
+        for i in range(k):
+            v = rng.normal(size=length)
+            v /= np.linalg.norm(v)
+            vs[i] = v
+        yield vs
+        done += k
+
+
+def gen_factor_device(lam, seed: int, tanh_max: float = 0.1):
+    """``gen_factor`` on the GPU: (G, signature) with G the column-major
+    device storage (an (n, n) tensor whose row i is column i of the factor).
+    Same draws and operation order as the reference; the reflector
+    applications run as FP64 rank-1 updates on the device."""
+    import torch
+
+    lam_sorted, n_plus = canonical_sort(lam)
+    n = lam_sorted.size
+    rng = np.random.Generator(np.random.PCG64(seed))
+    dev = torch.device("cuda")
+    # gt = g^T (row i of gt = column i of g)
+    gt = torch.diag(torch.as_tensor(np.sqrt(np.abs(lam_sorted)), device=dev))
+    # g <- H g  <=>  gt <- gt H:  gt -= 2 (gt v) v^T
+    for vs in _unit_reflectors(rng, n, n):
+        vd = torch.as_tensor(vs, device=dev)
+        for v in vd:
+            gt.addr_(gt @ v, v, alpha=-2.0)
+    # class blocks: g[:, lo:hi] <- (H block^T)^T, i.e. gt[lo:hi] <- H gt[lo:hi]
+    for lo, hi in ((0, n_plus), (n_plus, n)):
+        width = hi - lo
+        if width < 2:
+            continue
+        blk = gt[lo:hi]
+        for vs in _unit_reflectors(rng, width, width):
+            vd = torch.as_tensor(vs, device=dev)
+            for v in vd:
+                blk.addr_(v, v @ blk, alpha=-2.0)
+    if 0 < n_plus < n:
+        for _ in range(2 * n):
+            i = int(rng.integers(0, n_plus))
+            j = int(rng.integers(n_plus, n))
+            th = tanh_max * (2.0 * rng.random() - 1.0)
+            ch = 1.0 / math.sqrt(1.0 - th * th)
+            gi = gt[i].clone()
+            gj = gt[j].clone()
+            gt[i] = ch * (gi + th * gj)
+            gt[j] = ch * (th * gi + gj)
+    return gt.contiguous(), Signature(n, n_plus)
+
+
 def random_orthogonal_device(n: int, seed: int, m: int | None = None):
     """m x n (default n x n) matrix with orthonormal columns, FP64 on the GPU."""
     import torch
@@ -99,9 +207,9 @@ def random_orthogonal_device(n: int, seed: int, m: int | None = None):
     return q
 
 
-def gen_factor_device(sigma, seed: int, m: int | None = None):
-    """G = Q diag(sigma) W^T (m x n, FP64, on the GPU) returned in
-    column-major storage as an (n, m) tensor."""
+def gen_factor_orth_device(sigma, seed: int, m: int | None = None):
+    """G = Q diag(sigma) W^T (m x n, FP64, on the GPU, Haar Q and W) returned
+    in column-major storage as an (n, m) tensor."""
     import torch
 
     sig = torch.as_tensor(np.asarray(sigma, dtype=np.float64), device="cuda")
