@@ -73,7 +73,8 @@ def workload(args) -> dict:
         "outer_strategy": args.strategy, "inner_strategy": args.strategy,
         "input": (f"G = Q diag(sqrt(lambda)) W^T, lambda = type-{args.spectrum_type} spectrum "
                   f"(seed {args.seed}), Haar Q, W (GPU QR)"),
-        "l2": "inputs larger than L2 (factor 2 GiB per step)",
+        "l2": (f"inputs larger than L2 (factor {8 * args.n * args.n / 2**30:.2f} GiB per step)"
+               if 8 * args.n * args.n > 126e6 else "factor fits in L2 (no flush)"),
     }
 
 
@@ -229,6 +230,43 @@ def run_reference(args, rank: int):
     _ = O
 
 
+FP64_DMMA_PEAK_TF = 37.0  # measured: profiles/r01/dmma_chains_probe.jsonl (mma.sync f64, 8 warps/SM)
+
+
+def _init_dist(world: int):
+    """One process per GPU (torchrun): NCCL group, device = LOCAL_RANK."""
+    import torch
+    import torch.distributed as dist
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return dist
+
+
+def _max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _barrier(world: int):
+    import torch
+
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        torch.cuda.synchronize()
+
+
 def run_ours(args, rank: int, world: int):
     import torch
 
@@ -236,51 +274,98 @@ def run_ours(args, rank: int, world: int):
     from paper_1401_2720_b200.driver import Solver, SolverConfig
     import paper_1401_2720_b200 as J
 
-    if world > 1:
-        raise SystemExit("multi-GPU bench: use the distributed path (not in this build)")
+    _init_dist(world)
     lib = _lib.require_cuda()
     cfg = SolverConfig(block_width=args.width, variant=args.variant,
                        outer_strategy=args.strategy, inner_strategy=args.strategy)
     G0, sigma_true, n_plus = make_input(args)
     n = m = args.n
-    solver = Solver(n, cfg, J.Signature(n, n_plus))
-    eng = solver.engine
+    solver = Solver(n, cfg, J.Signature(n, n_plus)) if world == 1 else None
+    eng = solver.engine if solver else None
+
+    def solve():
+        """One step: a full solve from the resident factor.  N > 1: the
+        outer (multi-GPU) level of the reference, g = N workers, one per
+        rank, block-column exchange over NCCL (distsim.run_distributed)."""
+        if world == 1:
+            return solver.solve_device(G0)
+        from paper_1401_2720_b200.distsim import run_distributed
+
+        res, _ = run_distributed(G0.t(), J.Signature(n, n_plus), world, cfg)
+        return res
 
     # warm-up steps (full solves)
     for _ in range(args.warmup):
-        out = solver.solve_device(G0)
+        out = solve()
         del out
-    torch.cuda.synchronize()
+    _barrier(world)
 
     # timed steps
-    sampler = ClockSampler(torch.cuda.current_device())
-    sampler.start()
+    sampler = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
+    if sampler:
+        sampler.start()
     launches0 = lib.jh_launch_count()
-    nlaunch_cap = 4 * (eng.nsteps + 8) * cfg.max_block_sweeps * args.steps
+    nlaunch_cap = 4 * (n // (args.width // 2) + 8) * cfg.max_block_sweeps * args.steps * 4
     lib.jh_profile_begin(nlaunch_cap)
     times = []
     rotated_tasks = 0
-    gram_launches = 0
     res = None
     for _ in range(args.steps):
-        torch.cuda.synchronize()
+        _barrier(world)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        res = solver.solve_device(G0)
+        res = solve()
         e1.record()
-        torch.cuda.synchronize()
-        times.append(e0.elapsed_time(e1) / 1e3)
-        rotated_tasks += sum(eng.tasks_rotated)
-        gram_launches += len(res[3]) * eng.nsteps
+        _barrier(world)
+        times.append(_max_over_ranks(e0.elapsed_time(e1) / 1e3, world))
+        if eng is not None:
+            rotated_tasks += sum(eng.tasks_rotated)
     import ctypes
 
-    ms = (ctypes.c_double * 3)()
-    cnt = (ctypes.c_int64 * 3)()
+    ms = (ctypes.c_double * 4)()
+    cnt = (ctypes.c_int64 * 4)()
     lib.jh_profile_end(ms, cnt)
     launches = lib.jh_launch_count() - launches0
-    clocks = sampler.stop()
-    sigma, U, V, stats, converged = res
+    clocks = sampler.stop() if sampler else None
+    if world == 1:
+        sigma, U, V, stats, converged = res
+    else:
+        def dev_t(x):
+            return x if torch.is_tensor(x) else torch.as_tensor(np.asarray(x))
+        sigma = dev_t(res.sigma).cuda()
+        U = dev_t(res.u).cuda().t()  # (n, m) column-major storage like solve_device
+        V = dev_t(res.v).cuda().t()
+        stats, converged = [list(s) for s in res.stats], res.converged
     value = statistics.mean(times)
+
+    def run_e2e(G0):
+        """The same solve through the public API from pinned host memory
+        (host->device copy of the factor and device->host copy of sigma, U,
+        V inside the timed region); collective for N > 1."""
+        host_in = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
+        host_in.copy_(G0)
+        g_host = host_in.t()  # m x n, column-major, pinned
+        torch.cuda.empty_cache()
+        et = []
+        for _ in range(args.steps):
+            _barrier(world)
+            t0 = time.perf_counter()
+            if world == 1:
+                r = J.block_jacobi(g_host, J.Signature(n, n_plus), cfg)
+            else:
+                from paper_1401_2720_b200.distsim import run_distributed
+
+                r, _ = run_distributed(g_host, J.Signature(n, n_plus), world, cfg)
+            et.append(_max_over_ranks(time.perf_counter() - t0, world))
+            del r
+        return {"value": statistics.mean(et), "unit": "s", "h2d_bytes_per_step": 8 * m * n,
+                "d2h_bytes_per_step": 8 * (n + m * n + n * n)}
+
+    if rank != 0:
+        del U, V, res
+        if not args.no_e2e:
+            run_e2e(G0)
+        return
 
     # roofline of the dominant streaming kernel
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
@@ -311,6 +396,24 @@ def run_ours(args, rank: int, world: int):
         tj = json.loads(tp.read_text())
         traffic = tj.get(dom)
         traffic_alg = tj.get(dom + "_algorithmic")
+    # FP64 tensor-pipe (DMMA) roofline of the whole solve: algorithmic flops
+    # (Gram m w(w+1) per task and p-step, update 2 w^2 (m + n) per rotated
+    # task, Cholesky w^3/3 per task and p-step) over the solve time
+    chol_flops = ntask * w ** 3 / 3.0 * cnt[0]
+    solve_flops = classes["gram"]["flops_total"] + classes["update"]["flops_total"] + chol_flops
+    fp64 = {
+        "achieved_tflops": solve_flops / sum(times) / 1e12 if times else 0.0,
+        "peak_tflops": FP64_DMMA_PEAK_TF,
+        "frac": solve_flops / sum(times) / 1e12 / FP64_DMMA_PEAK_TF if times else 0.0,
+        "solve_flops": solve_flops,
+        "gram_tflops": (classes["gram"]["flops_total"] / (classes["gram"]["ms"] / 1e3) / 1e12
+                        if classes["gram"]["ms"] > 0 else None),
+        "update_tflops": (classes["update"]["flops_total"] / (classes["update"]["ms"] / 1e3)
+                          / 1e12 if classes["update"]["ms"] > 0 else None),
+        "peak_source": "measured DMMA rate, profiles/r01/dmma_chains_probe.jsonl",
+        "note": ("per-kernel rates from CUDA events around each launch; under sw_power_cap "
+                 "the SM clock (see clocks) scales the attainable peak"),
+    }
     roofline = {
         "kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
         "frac": achieved / hbm_peak, "traffic": traffic,
@@ -339,7 +442,7 @@ def run_ours(args, rank: int, world: int):
     # CPU baseline (bounded oracle sample) + bitwise prefix parity
     cpu = None
     parity = None
-    if not args.no_cpu:
+    if not args.no_cpu and world == 1:
         host = G0.cpu().numpy()
         t_p, k, threads, g_or, v_or = cpu_sample(host, args, args.cpu_seconds)
         b = n // (w // 2)
@@ -358,22 +461,8 @@ def run_ours(args, rank: int, world: int):
         del Gp, Vp, host, g_or, v_or
 
     # end to end through the public API with host buffers
-    e2e = None
-    if not args.no_e2e:
-        host_in = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
-        host_in.copy_(G0)
-        g_host = host_in.t()  # m x n, column-major, pinned
-        del G0
-        torch.cuda.empty_cache()
-        et = []
-        for _ in range(args.steps):
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            r = J.block_jacobi(g_host, J.Signature(n, n_plus), cfg)
-            et.append(time.perf_counter() - t0)
-            del r
-        e2e = {"value": statistics.mean(et), "unit": "s", "h2d_bytes_per_step": 8 * m * n,
-               "d2h_bytes_per_step": 8 * (n + m * n + n * n)}
+    e2e = run_e2e(G0) if not args.no_e2e else None
+    del G0
 
     line = {
         "metric": METRIC, "value": value, "unit": "s", "n_gpus": args.gpus,
@@ -383,7 +472,7 @@ def run_ours(args, rank: int, world: int):
         "dtype": "f64", "data": "synthetic", "config": workload(args),
         "sweeps": len(stats), "converged": converged, "stats": stats,
         "accuracy": accuracy, "parity_prefix": parity,
-        "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
+        "e2e": e2e, "roofline": roofline, "fp64_roofline": fp64, "cpu_baseline": cpu,
         "clocks": clocks, "gpu_launches": int(launches),
         "per_step_s": times,
     }
