@@ -1015,6 +1015,222 @@ __global__ void __launch_bounds__(kCyThreads, 2) k_update4(U4Args a) {
   u4_stream(S, A, ld, J);
 }
 
+// ---- engine 1, v2: persistent static-schedule update kernel -------------------
+//
+// The same items as k_update4 (G items of p-step s, V items of a p-step
+// pair), but one CTA per SM that walks items b, b + grid, ... with a
+// dedicated TMA producer warp running ahead across item boundaries: it
+// stages the next item's V' (double-buffered) and chunks (3-stage ring of
+// 64 rows x 64 columns) while the four DMMA warps finish the current one.
+
+struct U5Smem {
+  double ring[kCyStages - 1][kCyCols][kLd];   // 3 stages
+  double vp[2][4][kCyW][kCyVpLd];             // V' of two items in flight
+  CyV prm[2];
+  int64_t gcol[2][4];
+  int isv[2];
+  uint64_t full[kCyStages - 1], empty[kCyStages - 1];
+  uint64_t pfull[2], pempty[2];
+};
+constexpr int kU5Stages = kCyStages - 1;
+constexpr int kU5Threads = 160;
+
+// parameters of item `it` (the k_update4 interleave of G and V items)
+__device__ void u4_item(const U4Args &a, int it, CyV &J, const double *(&src)[4], bool &isV) {
+  const int N = a.nG + a.nV;
+  const int64_t v0 = (int64_t)it * a.nV / N, v1 = (int64_t)(it + 1) * a.nV / N;
+  isV = v1 > v0;
+  const int64_t WW = (int64_t)kCyW * kCyW;
+  src[0] = src[1] = src[2] = src[3] = nullptr;
+  if (!isV) {
+    const int i = it - (int)v0;
+    const int c = i % a.ncyc, k = i / a.ncyc;
+    const int32_t *cy = a.cyc + ((int64_t)((a.sg + 1) % a.S) * a.ncyc + c) * 8;
+    const int t1 = cy[0], t2 = cy[1];
+    const int32_t *pa = a.outer + ((int64_t)a.sg * a.T + t1) * 2;
+    const int32_t *pb = a.outer + ((int64_t)a.sg * a.T + t2) * 2;
+    J.blk[0] = pa[0];
+    J.blk[1] = pa[1];
+    J.blk[2] = pb[0];
+    J.blk[3] = pb[1];
+    J.upd[0] = a.rotG[t1] > 0;
+    J.upd[1] = a.rotG[t2] > 0;
+    J.second = false;
+    J.updB[0] = J.updB[1] = false;
+    J.ij[0][0] = J.ij[0][1] = J.ij[1][0] = J.ij[1][1] = 0;
+    J.r0 = (int64_t)k * kCyVSlab;
+    J.r1 = min64(J.r0 + kCyVSlab, a.m);
+    src[0] = a.VpG + t1 * WW;
+    src[1] = a.VpG + t2 * WW;
+    return;
+  }
+  int i = (int)v0, q = 0;
+  if (a.nsrc > 1 && i >= a.ncyc * a.vs[0].nk) {
+    i -= a.ncyc * a.vs[0].nk;
+    q = 1;
+  }
+  const U4Src &v = a.vs[q];
+  const int c = i % a.ncyc, k = v.k0 + (i / a.ncyc) * v.kstep;
+  const int32_t *cy = a.cyc + ((int64_t)((v.sa + 1) % a.S) * a.ncyc + c) * 8;
+  const int t1 = cy[0], t2 = cy[1];
+  const int32_t *pa = a.outer + ((int64_t)v.sa * a.T + t1) * 2;
+  const int32_t *pb = a.outer + ((int64_t)v.sa * a.T + t2) * 2;
+  J.blk[0] = pa[0];
+  J.blk[1] = pa[1];
+  J.blk[2] = pb[0];
+  J.blk[3] = pb[1];
+  J.upd[0] = v.rotA[t1] > 0;
+  J.upd[1] = v.rotA[t2] > 0;
+  J.second = v.second;
+  J.updB[0] = v.second && v.rotB[cy[2]] > 0;
+  J.updB[1] = v.second && v.rotB[cy[3]] > 0;
+  J.ij[0][0] = cy[4];
+  J.ij[0][1] = cy[5];
+  J.ij[1][0] = cy[6];
+  J.ij[1][1] = cy[7];
+  J.r0 = (int64_t)k * kCyVSlab;
+  J.r1 = min64(J.r0 + kCyVSlab, a.nv);
+  src[0] = v.VpA + t1 * WW;
+  src[1] = v.VpA + t2 * WW;
+  if (v.second) {
+    src[2] = v.VpB + cy[2] * WW;
+    src[3] = v.VpB + cy[3] * WW;
+  }
+}
+
+__global__ void __launch_bounds__(kU5Threads, 1) k_update5(U4Args a) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  U5Smem &S = *reinterpret_cast<U5Smem *>(smraw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int N = a.nG + a.nV;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kU5Stages; i++) {
+      mbar_init(&S.full[i], 1);
+      mbar_init(&S.empty[i], 4);
+    }
+    for (int i = 0; i < 2; i++) {
+      mbar_init(&S.pfull[i], 1);
+      mbar_init(&S.pempty[i], 4);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == 0) {
+    // ---- producer: V' + parameters per item, then the item's chunks
+    fence_async_global();
+    unsigned gc = 0;
+    int k = 0;
+    for (int it = blockIdx.x; it < N; it += gridDim.x, k++) {
+      const int slot = k & 1;
+      if (k >= 2) mbar_wait(&S.pempty[slot], ((k >> 1) - 1) & 1);
+      CyV J;
+      const double *src[4];
+      bool isV;
+      u4_item(a, it, J, src, isV);
+      double *A = isV ? a.V : a.G;
+      const int64_t ld = isV ? a.ldv : a.ldg;
+      const bool use[4] = {J.upd[0], J.upd[1], J.updB[0], J.updB[1]};
+      const bool any = use[0] || use[1] || use[2] || use[3];
+      if (!any) J.r1 = J.r0;  // nothing to do: no chunks
+      int nuse = 0;
+      for (int i = 0; i < 4; i++) nuse += use[i];
+      if (lane == 0) {
+        S.prm[slot] = J;
+        S.isv[slot] = isV;
+        for (int b = 0; b < 4; b++) S.gcol[slot][b] = (int64_t)J.blk[b] * 16;
+        mbar_expect_tx(&S.pfull[slot], (uint32_t)nuse * kCyW * kCyW * 8u);
+      }
+      __syncwarp();
+      // V' columns: 32 columns of 256 B per transform (padded stride in smem)
+      for (int i = 0; i < 4; i++)
+        if (use[i]) bulk_g2s(&S.vp[slot][i][lane][0], src[i] + lane * kCyW, kCyW * 8u, &S.pfull[slot]);
+      const int nchunk = (int)cdiv(J.r1 - J.r0, kRch);
+      for (int c = 0; c < nchunk; c++, gc++) {
+        const int st = (int)(gc % kU5Stages);
+        if (gc >= (unsigned)kU5Stages) mbar_wait(&S.empty[st], ((gc / kU5Stages) - 1) & 1);
+        const int64_t r = J.r0 + (int64_t)c * kRch;
+        const uint32_t bytes = (uint32_t)min64(kRch, J.r1 - r) * 8u;
+        if (lane == 0) mbar_expect_tx(&S.full[st], bytes * kCyCols);
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int j = lane + 32 * h;
+          const int64_t col = (int64_t)J.blk[j >> 4] * 16 + (j & 15);
+          bulk_g2s(&S.ring[st][j][0], A + col * ld + r, bytes, &S.full[st]);
+        }
+      }
+    }
+    return;
+  }
+  // ---- consumers: warp w owns rows 16 (w - 1) .. +16 of every chunk
+  const int cw = warp - 1;
+  unsigned gc = 0;
+  int k = 0;
+  for (int it = blockIdx.x; it < N; it += gridDim.x, k++) {
+    const int slot = k & 1;
+    mbar_wait(&S.pfull[slot], (k >> 1) & 1);
+    const CyV &J = S.prm[slot];
+    const bool isV = S.isv[slot] != 0;
+    double *A = isV ? a.V : a.G;
+    const int64_t ld = isV ? a.ldv : a.ldg;
+    int64_t gcol[4];
+#pragma unroll
+    for (int b = 0; b < 4; b++) gcol[b] = S.gcol[slot][b];
+    unsigned finB = 0;
+    if (J.second) {
+      if (J.updB[0]) finB |= (1u << J.ij[0][0]) | (1u << J.ij[0][1]);
+      if (J.updB[1]) finB |= (1u << J.ij[1][0]) | (1u << J.ij[1][1]);
+    }
+    const unsigned finA = 0xFu & ~finB;
+    const bool keepA = finB != 0;
+    const bool updA0 = J.upd[0], updA1 = J.upd[1], updB0 = J.second && J.updB[0],
+               updB1 = J.second && J.updB[1];
+    const int ib00 = 16 * J.ij[0][0], ib01 = 16 * J.ij[0][1];
+    const int ib10 = 16 * J.ij[1][0], ib11 = 16 * J.ij[1][1];
+    const int64_t r0 = J.r0, r1 = J.r1;
+    const int nchunk = (int)cdiv(r1 - r0, kRch);
+    for (int c = 0; c < nchunk; c++, gc++) {
+      const int st = (int)(gc % kU5Stages);
+      mbar_wait(&S.full[st], (gc / kU5Stages) & 1);
+      double *buf = &S.ring[st][0][0];
+      const int64_t r = r0 + (int64_t)c * kRch;
+      const int nr = (int)min64(kRch, r1 - r);
+      if (updA0)
+        u4_transform(buf, 16 * cw, 0, 16, &S.vp[slot][0][0][0], A, ld, gcol, finA, keepA, r, nr,
+                     g, t);
+      if (updA1)
+        u4_transform(buf, 16 * cw, 32, 48, &S.vp[slot][1][0][0], A, ld, gcol, finA, keepA, r,
+                     nr, g, t);
+      if (updB0 || updB1) __syncwarp();
+      if (updB0)
+        u4_transform(buf, 16 * cw, ib00, ib01, &S.vp[slot][2][0][0], A, ld, gcol, 0xFu, false, r,
+                     nr, g, t);
+      if (updB1)
+        u4_transform(buf, 16 * cw, ib10, ib11, &S.vp[slot][3][0][0], A, ld, gcol, 0xFu, false, r,
+                     nr, g, t);
+      if (keepA) fence_async_smem();  // generic writes before the slot's next TMA fill
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.empty[st]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.pempty[slot]);
+  }
+}
+
+void launch_update5(const U4Args &a, cudaStream_t st) {
+  const size_t smem = sizeof(U5Smem);
+  static int grid = 0;
+  if (!grid) {
+    cudaFuncSetAttribute(k_update5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    grid = sms;
+  }
+  const int N = a.nG + a.nV;
+  k_update5<<<N < grid ? N : grid, kU5Threads, smem, st>>>(a);
+}
+
 void launch_update4(double *G, int64_t ldg, int64_t m, double *V, int64_t ldv, int64_t nv,
                     const int32_t *outer, const int32_t *plan, int b, int sg, const double *VpG,
                     const int64_t *rotG, int nsrc, const int *sa, const bool *second,
@@ -1057,6 +1273,14 @@ void launch_update4(double *G, int64_t ldg, int64_t m, double *V, int64_t ldv, i
     a.nsrc++;
   }
   if (a.nG + a.nV == 0) return;
+  static const int v5 = [] {
+    const char *e = getenv("JHSVD_U4");  // "1": the one-item-per-CTA kernel
+    return !(e && e[0] == '1');
+  }();
+  if (v5) {
+    launch_update5(a, st);
+    return;
+  }
   const size_t smem = sizeof(CySmem);
   static bool attr = false;
   if (!attr) {
