@@ -212,7 +212,7 @@ def gen_factor_orth_device(sigma, seed: int, m: int | None = None):
     in column-major storage as an (n, m) tensor."""
     import torch
 
-    sig = torch.as_tensor(np.asarray(sigma, dtype=np.float64), device="cuda")
+    sig = torch.as_tensor(np.ascontiguousarray(sigma, dtype=np.float64), device="cuda")
     n = sig.numel()
     m = n if m is None else m
     q = random_orthogonal_device(n, seed, m)
