@@ -78,6 +78,10 @@ k_gram_tma(const double *__restrict__ G, int64_t ldg, int64_t m,
       gram_chunk<W, NW, 0>(buf, nr, acc, t);
     else if (NW > 1 && cw == 1)
       gram_chunk<W, NW, (NW > 1 ? 1 : 0)>(buf, nr, acc, t);
+    else if (NW > 2 && cw == 2)
+      gram_chunk<W, NW, (NW > 2 ? 2 : 0)>(buf, nr, acc, t);
+    else if (NW > 3 && cw == 3)
+      gram_chunk<W, NW, (NW > 3 ? 3 : 0)>(buf, nr, acc, t);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
@@ -86,6 +90,10 @@ k_gram_tma(const double *__restrict__ G, int64_t ldg, int64_t m,
     gram_store<W, NW, 0>(H, acc, g, t);
   else if (NW > 1 && cw == 1)
     gram_store<W, NW, (NW > 1 ? 1 : 0)>(H, acc, g, t);
+  else if (NW > 2 && cw == 2)
+    gram_store<W, NW, (NW > 2 ? 2 : 0)>(H, acc, g, t);
+  else if (NW > 3 && cw == 3)
+    gram_store<W, NW, (NW > 3 ? 3 : 0)>(H, acc, g, t);
 }
 
 // ---------------------------------------------------------------------------
@@ -289,20 +297,41 @@ bool gram_tma_ok(int w, int64_t m, int64_t ldg) {
   return (w == 16 || w == 32) && m % 2 == 0 && ldg % 2 == 0;
 }
 
-constexpr int kGramWarps = 2;
+// consumer warps per Gram CTA: 2 (tiles 5 + 5 for w = 32), or 4 when few
+// tasks meet long columns (tall factors: one CTA per task leaves SMs short
+// of DMMA warps while every tile is a chain over all m rows); JHSVD_GRAM_NW
+// overrides
+template <int W, int NW>
+static void launch_gram_nw(const double *G, int64_t ldg, int64_t m, const int32_t *pairs,
+                           int ntask, double *Hbuf, cudaStream_t st) {
+  const size_t smem = sizeof(double) * (size_t)kStages * W * kLd;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_gram_tma<W, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr = true;
+  }
+  k_gram_tma<W, NW><<<ntask, 32 * (NW + 1), smem, st>>>(G, ldg, m, pairs, Hbuf);
+}
 
 template <int W>
 static void launch_gram_t(const double *G, int64_t ldg, int64_t m, const int32_t *pairs,
                           int ntask, double *Hbuf, cudaStream_t st) {
-  const size_t smem = sizeof(double) * (size_t)kStages * W * kLd;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_gram_tma<W, kGramWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    attr = true;
+  static const int env_nw = [] {
+    const char *e = getenv("JHSVD_GRAM_NW");
+    return e ? atoi(e) : 0;
+  }();
+  int nw = env_nw;
+  if (nw != 2 && nw != 4) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    nw = (ntask < 3 * sms) ? 4 : 2;
   }
-  k_gram_tma<W, kGramWarps><<<ntask, 32 * (kGramWarps + 1), smem, st>>>(G, ldg, m, pairs,
-                                                                       Hbuf);
+  if (nw == 4)
+    launch_gram_nw<W, 4>(G, ldg, m, pairs, ntask, Hbuf, st);
+  else
+    launch_gram_nw<W, 2>(G, ldg, m, pairs, ntask, Hbuf, st);
 }
 
 void launch_gram_tma(const double *G, int64_t ldg, int64_t m, const int32_t *pairs, int ntask,
