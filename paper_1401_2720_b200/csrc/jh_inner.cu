@@ -746,165 +746,6 @@ k_factor_inner4(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
   }
 }
 
-// ===========================================================================
-// K2+K3 fused (W = 16, 32): inner Jacobi, then -- in the same CTA -- the
-// post-multiplication of the task's pair columns of G and V by V'.
-//
-// All tasks of a p-step are resident at once (29 KB of shared memory and 96
-// threads per CTA), so a task whose inner sweeps converge early starts
-// streaming its update while slower tasks are still rotating: the
-// latency-bound inner phase hides under the HBM-bound update instead of
-// adding to it.  Update: warp 0 streams 32-row chunks of the pair (G rows,
-// then V rows) through a 3-stage TMA ring that reuses the inner phase's
-// shared memory; warps 1-2 each rotate 16 rows per chunk with DMMA against
-// V' fragments held in registers, storing straight to global memory.
-
-constexpr int kFuRows = 32;
-constexpr int kFuLd = kFuRows + 4;   // == 4 (mod 16): conflict-free fragment loads
-constexpr int kFuStages = 3;
-constexpr int kFuCons = 2;
-constexpr int kFuThreads = 32 * (1 + kFuCons);
-
-template <int W>
-struct FusedSmem {
-  union {
-    Inner4Smem<W> in;
-    double ring[kFuStages][W][kFuLd];
-  } u;
-  uint64_t full[kFuStages], empty[kFuStages];
-};
-
-template <int W>
-__global__ void __launch_bounds__(kFuThreads)
-k_inner_update(double *__restrict__ G, int64_t ldg, int64_t m, double *__restrict__ Vm,
-               int64_t ldv, int64_t nv, const double *__restrict__ Hbuf,
-               int64_t *__restrict__ task_rot, const int32_t *__restrict__ pairs,
-               int64_t n_plus, const int32_t *__restrict__ inner, int inner_limit,
-               double tol_c, unsigned long long *counters, int pstep, int task_base) {
-  constexpr int NT = W / 8, NK = W / 4, BW = W / 2, LDV = W + 1;
-  extern __shared__ __align__(128) unsigned char smraw[];
-  FusedSmem<W> &S = *reinterpret_cast<FusedSmem<W> *>(smraw);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
-  const int task = blockIdx.x;
-  if (!inner4_body<W, kFuThreads>(S.u.in, Hbuf, task_rot, pairs, n_plus, inner, inner_limit,
-                                  tol_c, counters, pstep, task_base, task))
-    return;
-  if (S.u.in.tot_rot == 0) return;  // no rotation: columns unchanged (driver.py:165)
-  const int p = pairs[2 * task], q = pairs[2 * task + 1];
-  double bf[NK][NT];
-  if (warp >= 1) {
-#pragma unroll
-    for (int kk = 0; kk < NK; kk++)
-#pragma unroll
-      for (int Y = 0; Y < NT; Y++) bf[kk][Y] = S.u.in.V[(8 * Y + g) * LDV + 4 * kk + t];
-  }
-  if (tid == 0) {
-    for (int s = 0; s < kFuStages; s++) {
-      mbar_init(&S.full[s], 1);
-      mbar_init(&S.empty[s], kFuCons);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();  // V' is in registers; the inner phase's memory becomes the ring
-  const int ncg = (int)cdiv(m, kFuRows);
-  const int nc = ncg + (Vm ? (int)cdiv(nv, kFuRows) : 0);
-  auto chunk = [&](int c, double *&A, int64_t &ld, int64_t &rows, int64_t &r0) {
-    if (c < ncg) {
-      A = G; ld = ldg; rows = m; r0 = (int64_t)c * kFuRows;
-    } else {
-      A = Vm; ld = ldv; rows = nv; r0 = (int64_t)(c - ncg) * kFuRows;
-    }
-  };
-  if (warp == 0) {
-    for (int c = 0; c < nc; c++) {
-      const int s = c % kFuStages;
-      if (c >= kFuStages) mbar_wait(&S.empty[s], (uint32_t)(((c / kFuStages) - 1) & 1));
-      double *A;
-      int64_t ld, rows, r0;
-      chunk(c, A, ld, rows, r0);
-      const uint32_t bytes = (uint32_t)min64(kFuRows, rows - r0) * 8u;
-      if (lane == 0) mbar_expect_tx(&S.full[s], bytes * W);
-      __syncwarp();
-      for (int j = lane; j < W; j += 32) {
-        const int64_t col = j < BW ? (int64_t)p * BW + j : (int64_t)q * BW + (j - BW);
-        bulk_g2s(&S.u.ring[s][j][0], A + col * ld + r0, bytes, &S.full[s]);
-      }
-    }
-    return;
-  }
-  const int cw = warp - 1;
-  for (int c = 0; c < nc; c++) {
-    const int s = c % kFuStages;
-    mbar_wait(&S.full[s], (uint32_t)((c / kFuStages) & 1));
-    double *A;
-    int64_t ld, rows, r0;
-    chunk(c, A, ld, rows, r0);
-    double *pout = A + ((int64_t)p * BW + 2 * t) * ld;
-    double *qout = A + ((int64_t)q * BW + 2 * t) * ld;
-#pragma unroll
-    for (int rb = 0; rb < 2; rb++) {
-      const int rl = cw * 16 + rb * 8;
-      double a[NK];
-#pragma unroll
-      for (int kk = 0; kk < NK; kk++) a[kk] = S.u.ring[s][4 * kk + t][rl + g];
-      double acc[NT][2];
-#pragma unroll
-      for (int Y = 0; Y < NT; Y++) acc[Y][0] = acc[Y][1] = 0.0;
-#pragma unroll
-      for (int kk = 0; kk < NK; kk++)
-#pragma unroll
-        for (int Y = 0; Y < NT; Y++) dmma(acc[Y][0], acc[Y][1], a[kk], bf[kk][Y]);
-      const int64_t row = r0 + rl + g;
-      if (row < rows) {
-#pragma unroll
-        for (int Y = 0; Y < NT; Y++)
-#pragma unroll
-          for (int j = 0; j < 2; j++) {
-            double *dst = Y < NT / 2 ? pout + (int64_t)(8 * Y + j) * ld
-                                     : qout + (int64_t)(8 * Y + j - BW) * ld;
-            st_f64(dst + row, acc[Y][j]);
-          }
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&S.empty[s]);
-  }
-}
-
-bool fused_ok(int w, int64_t m, int64_t ldg, int64_t nv, int64_t ldv) {
-  return (w == 16 || w == 32) && m % 2 == 0 && ldg % 2 == 0 && nv % 2 == 0 && ldv % 2 == 0;
-}
-
-template <int W>
-static void launch_fused_t(double *G, int64_t ldg, int64_t m, double *V, int64_t ldv, int64_t nv,
-                           const double *Hbuf, int64_t *trot, const int32_t *pairs, int ntask,
-                           int64_t n_plus, const int32_t *inner, int inner_limit, double tol_c,
-                           unsigned long long *counters, int pstep, cudaStream_t st,
-                           int task_base) {
-  const size_t smem = sizeof(FusedSmem<W>);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_inner_update<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    attr = true;
-  }
-  k_inner_update<W><<<ntask, kFuThreads, smem, st>>>(G, ldg, m, V, ldv, nv, Hbuf, trot, pairs,
-                                                     n_plus, inner, inner_limit, tol_c, counters,
-                                                     pstep, task_base);
-}
-
-void launch_fused(double *G, int64_t ldg, int64_t m, double *V, int64_t ldv, int64_t nv,
-                  const double *Hbuf, int64_t *trot, const int32_t *pairs, int ntask, int w,
-                  int64_t n_plus, const int32_t *inner, int inner_limit, double tol_c,
-                  unsigned long long *counters, int pstep, cudaStream_t st, int task_base) {
-  if (w == 16)
-    launch_fused_t<16>(G, ldg, m, V, ldv, nv, Hbuf, trot, pairs, ntask, n_plus, inner,
-                       inner_limit, tol_c, counters, pstep, st, task_base);
-  else
-    launch_fused_t<32>(G, ldg, m, V, ldv, nv, Hbuf, trot, pairs, ntask, n_plus, inner,
-                       inner_limit, tol_c, counters, pstep, st, task_base);
-}
-
 bool inner4_ok(int w) { return w == 16 || w == 32; }
 
 template <int W>

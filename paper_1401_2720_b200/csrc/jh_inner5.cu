@@ -1,7 +1,9 @@
-// Variant 5 of K2 (kept for A/B timing): the v3 inner Jacobi as first
-// written -- one CTA of 4 warps per task, pairs' dot products by w/2 lanes of
-// warp 0, R applied by all threads one pair at a time, V applied by warps 1-3
-// one inner p-step behind.  Same arithmetic as every other variant.
+// K2, the default inner Jacobi kernel (variant 5; fastest at n = 16384 in
+// tools/bench_inner.py): one CTA of 4 warps per task, pairs' dot products
+// by w/2 lanes of warp 0, R applied by all threads one pair at a time, V
+// applied by warps 1-3 one inner p-step behind (jh_inner5.cuh).  Variants 3
+// and 4 (jh_inner.cu) give bitwise the same results and stay for A/B runs
+// (JHSVD_INNER=3/4).
 #include "jh_inner5.cuh"
 #include "jh_kernels.h"
 

@@ -31,13 +31,6 @@ void launch_inner4(const double *Hbuf, double *Vbuf, int64_t *trot, const int32_
                    double tol_c, unsigned long long *counters, int pstep, cudaStream_t st,
                    int task_base = 0);
 
-// fused inner Jacobi + post-multiplication per task, w in {16, 32} (jh_inner.cu)
-bool fused_ok(int w, int64_t m, int64_t ldg, int64_t nv, int64_t ldv);
-void launch_fused(double *G, int64_t ldg, int64_t m, double *V, int64_t ldv, int64_t nv,
-                  const double *Hbuf, int64_t *trot, const int32_t *pairs, int ntask, int w,
-                  int64_t n_plus, const int32_t *inner, int inner_limit, double tol_c,
-                  unsigned long long *counters, int pstep, cudaStream_t st, int task_base = 0);
-
 // the first v3 inner Jacobi, kept for A/B timing (jh_inner5.cu)
 bool inner5_ok(int w);
 // from_r: Hbuf holds the shortened factors R (QR peel-off) instead of Grams

@@ -796,102 +796,6 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : -(int)e;
   }
-  // Optional: Gram kernel + fused (inner Jacobi -> post-multiply) kernel per
-  // p-step (JHSVD_FUSED=1).
-  static const char *env_fused = getenv("JHSVD_FUSED");
-  // (off by default: per task the update is confined to one SM, which makes
-  // the DMMA work per SM uneven; measured slower than the three kernels)
-  const bool fused = use_tma_gram && use_dmma_update && (env_fused && env_fused[0] == '1') &&
-                     fused_ok(w, m, ldg, V ? nv : 0, V ? ldv : 0);
-  if (fused) {
-    for (int s = first_step; s < first_step + nsteps; s++) {
-      const int32_t *pairs = outer + (int64_t)s * ntask * 2;
-      prof_mark(st, 0, false);
-      launch_gram_tma(G, ldg, m, pairs, ntask, w, Hbuf, st);
-      prof_mark(st, 0, true);
-      prof_mark(st, 1, false);
-      launch_fused(G, ldg, m, V, ldv, nv, Hbuf, trot, pairs, ntask, w, n_plus, inner,
-                   inner_limit, tol_c, counters, s, st);
-      prof_mark(st, 1, true);
-      g_launches += 2;
-    }
-    cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? 0 : -(int)e;
-  }
-  // K-way staggered pipeline of a p-step (JHSVD_STREAMS = K, 0/1 disables)
-  static const int env_k = [] {
-    const char *e = getenv("JHSVD_STREAMS");
-    return e ? atoi(e) : 0;
-  }();
-  const int K = (use_tma_gram && use_dmma_update && inner3_ok(w)) ? env_k : 0;
-  if (K >= 2 && ntask >= 16 * K) {
-    // The tasks of a p-step are split into K parts.  Part k's Gram follows
-    // part k-1's on one stream (so the Grams stream back to back at full
-    // bandwidth), its latency-bound inner Jacobi runs on its own
-    // high-priority stream as soon as its Gram is done, and its update
-    // follows its inner Jacobi.  The inner phases of all parts but the first
-    // thus run under other parts' streaming kernels.  The next p-step starts
-    // after all updates (block-columns move between parts across p-steps).
-    constexpr int KMAX = 8;
-    static cudaStream_t sP[KMAX], sI[KMAX];
-    static cudaEvent_t eG[KMAX], eI[KMAX], eU[KMAX], eStart, eJoin;
-    static bool init = false;
-    if (!init) {
-      int lo, hi;
-      cudaDeviceGetStreamPriorityRange(&lo, &hi);
-      for (int k = 0; k < KMAX; k++) {
-        cudaStreamCreateWithPriority(&sP[k], cudaStreamNonBlocking, lo);
-        cudaStreamCreateWithPriority(&sI[k], cudaStreamNonBlocking, hi);
-        cudaEventCreateWithFlags(&eG[k], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&eI[k], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&eU[k], cudaEventDisableTiming);
-      }
-      cudaEventCreateWithFlags(&eStart, cudaEventDisableTiming);
-      cudaEventCreateWithFlags(&eJoin, cudaEventDisableTiming);
-      init = true;
-    }
-    const int KK = K > KMAX ? KMAX : K;
-    const size_t ww = (size_t)w * w;
-    cudaEventRecord(eStart, st);
-    for (int k = 0; k < KK; k++) {
-      cudaStreamWaitEvent(sP[k], eStart, 0);
-      cudaStreamWaitEvent(sI[k], eStart, 0);
-    }
-    for (int s = first_step; s < first_step + nsteps; s++) {
-      const int32_t *pairs = outer + (int64_t)s * ntask * 2;
-      for (int k = 0; k < KK; k++) {
-        const int t0 = (int)((int64_t)ntask * k / KK);
-        const int nt = (int)((int64_t)ntask * (k + 1) / KK) - t0;
-        const int32_t *pr = pairs + 2 * t0;
-        cudaStream_t sx = sP[k], si = sI[k];
-        if (k > 0) cudaStreamWaitEvent(sx, eG[k - 1], 0);  // Grams back to back
-        prof_mark(sx, 0, false);
-        launch_gram_tma(G, ldg, m, pr, nt, w, Hbuf + t0 * ww, sx);
-        prof_mark(sx, 0, true);
-        cudaEventRecord(eG[k], sx);
-        cudaStreamWaitEvent(si, eG[k], 0);
-        prof_mark(si, 1, false);
-        launch_inner3(Hbuf + t0 * ww, Vbuf + t0 * ww, trot + t0, pr, nt, w, n_plus, inner,
-                      inner_limit, tol_c, counters, s, si, t0);
-        prof_mark(si, 1, true);
-        cudaEventRecord(eI[k], si);
-        cudaStreamWaitEvent(sx, eI[k], 0);
-        prof_mark(sx, 2, false);
-        launch_update_dmma(G, ldg, m, V, ldv, nv, pr, nt, w, Vbuf + t0 * ww, trot + t0, sx);
-        prof_mark(sx, 2, true);
-        cudaEventRecord(eU[k], sx);
-        g_launches += 3;
-      }
-      // join: every part of the next p-step waits for all updates
-      for (int k = 1; k < KK; k++) cudaStreamWaitEvent(sP[0], eU[k], 0);
-      cudaEventRecord(eJoin, sP[0]);
-      for (int k = 1; k < KK; k++) cudaStreamWaitEvent(sP[k], eJoin, 0);
-    }
-    cudaEventRecord(eJoin, sP[0]);
-    cudaStreamWaitEvent(st, eJoin, 0);
-    cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? 0 : -(int)e;
-  }
   for (int s = first_step; s < first_step + nsteps; s++) {
     const int32_t *pairs = outer + (int64_t)s * ntask * 2;
     prof_mark(st, 0, false);
