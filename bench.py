@@ -374,13 +374,17 @@ def run_ours(args, rank: int, world: int):
     w = args.width
     ntask = n // w
     bytes_gram_launch = ntask * 8.0 * w * m
-    bytes_update_total = rotated_tasks * 16.0 * w * (m + n)
+    # algorithmic HBM bytes of the update launches: read + write of the pair
+    # columns of G per rotated task; V the same per p-step (engine 0) or once
+    # per two p-steps over the 4-cycles of the pair (engine 1, jh_vpair.cu)
+    v_factor = 0.5 if (eng is not None and eng.engine == 1) else 1.0
+    bytes_update_total = rotated_tasks * 16.0 * w * (m + v_factor * n)
     classes = {
         "gram": {"ms": ms[0], "launches": cnt[0],
                  "bytes_total": bytes_gram_launch * cnt[0],
                  "flops_total": ntask * m * w * (w + 1.0) * cnt[0]},
         "factor_inner": {"ms": ms[1], "launches": cnt[1], "bytes_total": 0.0},
-        "update": {"ms": ms[2], "launches": cnt[2], "bytes_total": bytes_update_total,
+        "update": {"ms": ms[2] + ms[3], "launches": cnt[2], "bytes_total": bytes_update_total,
                    "flops_total": rotated_tasks * 2.0 * w * w * (m + n)},
     }
     tot_ms = sum(c["ms"] for c in classes.values()) or 1.0

@@ -796,500 +796,6 @@ __global__ void k_cycle_init(CyArgs a) {
   }
 }
 
-// ---- combined update kernel of the per-p-step pipeline (engine 1) ---------------
-//
-// One launch per p-step s: the post-multiplication of the G block-columns of
-// every task of p-step s that rotated (driver.py:165-172), and -- deferred --
-// the V post-multiplications of a pair of p-steps (a, a+1) in one pass over
-// V.  Both kinds of item stream four block-columns (two tasks) through a
-// 2-stage TMA ring: warp w owns rows 16 w .. 16 w + 15 of every 64-row chunk
-// and applies the item's transforms to them in place, with the tasks' V' in
-// shared memory, writing final values straight from the DMMA accumulators
-// to HBM.  G items are HBM-bound, V items (two transforms per row) DMMA-
-// bound; one grid interleaving both keeps both pipes busy.
-
-struct U4Src {
-  int sa;                     // p-step a of the pair (a, a+1) (a alone if !second)
-  bool second;
-  const double *VpA, *VpB;
-  const int64_t *rotA, *rotB;
-  int k0, kstep, nk;          // V row slabs k0, k0 + kstep, ... (nk of them)
-};
-
-struct U4Args {
-  double *G;
-  int64_t ldg, m;
-  double *V;
-  int64_t ldv, nv;
-  const int32_t *outer, *cyc;
-  int S, T, ncyc;
-  int sg;                     // p-step of the G items (-1: none)
-  const double *VpG;
-  const int64_t *rotG;
-  int nslab_g, nG;            // G items: ncyc * nslab_g
-  U4Src vs[2];
-  int nsrc, nV;               // V items: sum over sources of ncyc * nk
-};
-
-// 16 rows (two row tiles) x the 32 slot columns col(k) = cb0 + k (k < 16),
-// cb1 + k - 16 (k >= 16), post-multiplied by V' in shared memory (ld
-// kCyVpLd); results to the slot in place (`keep`) and to HBM for the blocks
-// in `fin` (column gcol[b] + n, rows grow + row, nr valid rows).
-__device__ __forceinline__ void u4_transform(double *buf, int row0, int cb0, int cb1,
-                                             const double *vp, double *A, int64_t ld,
-                                             const int64_t (&gcol)[4], unsigned fin, bool keep,
-                                             int64_t grow, int nr, int g, int t) {
-  const int rb = row0 + g;
-  double acc[2][4][2];
-#pragma unroll
-  for (int rt = 0; rt < 2; rt++)
-#pragma unroll
-    for (int Y = 0; Y < 4; Y++) acc[rt][Y][0] = acc[rt][Y][1] = 0.0;
-#pragma unroll
-  for (int kk = 0; kk < 8; kk++) {
-    double b[4];
-#pragma unroll
-    for (int Y = 0; Y < 4; Y++) b[Y] = vp[(8 * Y + g) * kCyVpLd + 4 * kk + t];
-    const int col = (kk < 4 ? cb0 + 4 * kk : cb1 + 4 * kk - 16) + t;
-#pragma unroll
-    for (int rt = 0; rt < 2; rt++) {
-      const double av = buf[col * kLd + rb + 8 * rt];
-#pragma unroll
-      for (int Y = 0; Y < 4; Y++) dmma(acc[rt][Y][0], acc[rt][Y][1], av, b[Y]);
-    }
-  }
-  const int sw = (t >> 1) & 1;  // conflict-free 64-bit shared stores
-#pragma unroll
-  for (int rt = 0; rt < 2; rt++) {
-    const int row = rb + 8 * rt;
-#pragma unroll
-    for (int Y = 0; Y < 4; Y++) {
-      const int cbase = Y < 2 ? cb0 : cb1, blk = cbase >> 4;
-      const bool to_global = ((fin >> blk) & 1) && row < nr;
-#pragma unroll
-      for (int jj = 0; jj < 2; jj++) {
-        const int j = jj ^ sw;
-        const double v = j ? acc[rt][Y][1] : acc[rt][Y][0];
-        const int n = 8 * (Y & 1) + 2 * t + j;
-        if (keep) buf[(cbase + n) * kLd + row] = v;
-        if (to_global) st_f64(A + (gcol[blk] + n) * ld + grow + row, v);
-      }
-    }
-  }
-}
-
-__device__ __noinline__ void u4_stream(CySmem &S, double *A, int64_t ld, const CyV &J) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const int nchunk = (int)cdiv(J.r1 - J.r0, kRch);
-  const unsigned base = S.vchunk;
-  if (warp == 0) {
-    fence_async_global();
-    fence_async_smem();
-    for (int c = 0; c < kCyVStages - 1 && c < nchunk; c++) cy_issue_v(S, A, ld, J, base, c);
-  }
-  int64_t gcol[4];
-#pragma unroll
-  for (int b = 0; b < 4; b++) gcol[b] = (int64_t)J.blk[b] * 16;
-  unsigned finB = 0;
-  if (J.second) {
-    if (J.updB[0]) finB |= (1u << J.ij[0][0]) | (1u << J.ij[0][1]);
-    if (J.updB[1]) finB |= (1u << J.ij[1][0]) | (1u << J.ij[1][1]);
-  }
-  const unsigned finA = 0xFu & ~finB;
-  const bool keepA = finB != 0;  // transform B reads transform A's results
-  for (int c = 0; c < nchunk; c++) {
-    if (warp == 0 && c + kCyVStages - 1 < nchunk) cy_issue_v(S, A, ld, J, base, c + kCyVStages - 1);
-    const unsigned gc = base + c;
-    const int st = (int)(gc % kCyVStages);
-    mbar_wait(&S.vfull[st], (gc / kCyVStages) & 1);
-    double *buf = &S.u.v.ring[st][0][0];
-    const int64_t r = J.r0 + (int64_t)c * kRch;
-    const int nr = (int)min64(kRch, J.r1 - r);
-#pragma unroll 1
-    for (int h = 0; h < 2; h++)
-      if (J.upd[h])
-        u4_transform(buf, 16 * warp, 32 * h, 32 * h + 16, &S.u.v.vp[h][0][0], A, ld, gcol, finA,
-                     keepA, r, nr, g, t);
-    if (J.second) {
-      __syncwarp();
-#pragma unroll 1
-      for (int h = 0; h < 2; h++)
-        if (J.updB[h])
-          u4_transform(buf, 16 * warp, 16 * J.ij[h][0], 16 * J.ij[h][1], &S.u.v.vp[2 + h][0][0],
-                       A, ld, gcol, 0xFu, false, r, nr, g, t);
-    }
-    fence_async_smem();  // generic writes before the slot's next TMA fill
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&S.vempty[st]);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) S.vchunk = base + nchunk;
-  __syncthreads();
-}
-
-__global__ void __launch_bounds__(kCyThreads, 2) k_update4(U4Args a) {
-  extern __shared__ __align__(128) unsigned char smraw[];
-  CySmem &S = *reinterpret_cast<CySmem *>(smraw);
-  // interleave the two kinds of item over the grid
-  const int N = a.nG + a.nV, bid = blockIdx.x;
-  const int64_t v0 = (int64_t)bid * a.nV / N, v1 = (int64_t)(bid + 1) * a.nV / N;
-  const bool isV = v1 > v0;
-  const int64_t WW = (int64_t)kCyW * kCyW;
-  CyV J;
-  const double *src[4] = {nullptr, nullptr, nullptr, nullptr};
-  double *A;
-  int64_t ld;
-  if (!isV) {
-    const int i = bid - (int)v0;
-    const int c = i % a.ncyc, k = i / a.ncyc;
-    const int32_t *cy = a.cyc + ((int64_t)((a.sg + 1) % a.S) * a.ncyc + c) * 8;
-    const int t1 = cy[0], t2 = cy[1];
-    const int32_t *pa = a.outer + ((int64_t)a.sg * a.T + t1) * 2;
-    const int32_t *pb = a.outer + ((int64_t)a.sg * a.T + t2) * 2;
-    J.blk[0] = pa[0];
-    J.blk[1] = pa[1];
-    J.blk[2] = pb[0];
-    J.blk[3] = pb[1];
-    J.upd[0] = a.rotG[t1] > 0;
-    J.upd[1] = a.rotG[t2] > 0;
-    J.second = false;
-    J.updB[0] = J.updB[1] = false;
-    J.ij[0][0] = J.ij[0][1] = J.ij[1][0] = J.ij[1][1] = 0;
-    J.r0 = (int64_t)k * kCyVSlab;
-    J.r1 = min64(J.r0 + kCyVSlab, a.m);
-    src[0] = a.VpG + t1 * WW;
-    src[1] = a.VpG + t2 * WW;
-    A = a.G;
-    ld = a.ldg;
-  } else {
-    int i = (int)v0, q = 0;
-    if (a.nsrc > 1 && i >= a.ncyc * a.vs[0].nk) {
-      i -= a.ncyc * a.vs[0].nk;
-      q = 1;
-    }
-    const U4Src &v = a.vs[q];
-    const int c = i % a.ncyc, k = v.k0 + (i / a.ncyc) * v.kstep;
-    const int32_t *cy = a.cyc + ((int64_t)((v.sa + 1) % a.S) * a.ncyc + c) * 8;
-    const int t1 = cy[0], t2 = cy[1];
-    const int32_t *pa = a.outer + ((int64_t)v.sa * a.T + t1) * 2;
-    const int32_t *pb = a.outer + ((int64_t)v.sa * a.T + t2) * 2;
-    J.blk[0] = pa[0];
-    J.blk[1] = pa[1];
-    J.blk[2] = pb[0];
-    J.blk[3] = pb[1];
-    J.upd[0] = v.rotA[t1] > 0;
-    J.upd[1] = v.rotA[t2] > 0;
-    J.second = v.second;
-    J.updB[0] = v.second && v.rotB[cy[2]] > 0;
-    J.updB[1] = v.second && v.rotB[cy[3]] > 0;
-    J.ij[0][0] = cy[4];
-    J.ij[0][1] = cy[5];
-    J.ij[1][0] = cy[6];
-    J.ij[1][1] = cy[7];
-    J.r0 = (int64_t)k * kCyVSlab;
-    J.r1 = min64(J.r0 + kCyVSlab, a.nv);
-    src[0] = v.VpA + t1 * WW;
-    src[1] = v.VpA + t2 * WW;
-    if (v.second) {
-      src[2] = v.VpB + cy[2] * WW;
-      src[3] = v.VpB + cy[3] * WW;
-    }
-    A = a.V;
-    ld = a.ldv;
-  }
-  const bool use[4] = {J.upd[0], J.upd[1], J.updB[0], J.updB[1]};
-  if (J.r1 <= J.r0 || !(use[0] || use[1] || use[2] || use[3])) return;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kCyVStages; s++) {
-      mbar_init(&S.vfull[s], 1);
-      mbar_init(&S.vempty[s], 4);
-    }
-    fence_mbar_init();
-    S.vchunk = 0;
-  }
-  for (int e = threadIdx.x; e < 4 * kCyW * kCyW; e += blockDim.x) {
-    const int i = e / (kCyW * kCyW), rr = e - i * kCyW * kCyW;
-    if (use[i]) S.u.v.vp[i][rr / kCyW][rr % kCyW] = src[i][rr];
-  }
-  __syncthreads();
-  u4_stream(S, A, ld, J);
-}
-
-// ---- engine 1, v2: persistent static-schedule update kernel -------------------
-//
-// The same items as k_update4 (G items of p-step s, V items of a p-step
-// pair), but one CTA per SM that walks items b, b + grid, ... with a
-// dedicated TMA producer warp running ahead across item boundaries: it
-// stages the next item's V' (double-buffered) and chunks (3-stage ring of
-// 64 rows x 64 columns) while the four DMMA warps finish the current one.
-
-struct U5Smem {
-  double ring[kCyStages - 1][kCyCols][kLd];   // 3 stages
-  double vp[2][4][kCyW][kCyVpLd];             // V' of two items in flight
-  CyV prm[2];
-  int64_t gcol[2][4];
-  int isv[2];
-  uint64_t full[kCyStages - 1], empty[kCyStages - 1];
-  uint64_t pfull[2], pempty[2];
-};
-constexpr int kU5Stages = kCyStages - 1;
-constexpr int kU5Threads = 160;
-
-// parameters of item `it` (the k_update4 interleave of G and V items)
-__device__ void u4_item(const U4Args &a, int it, CyV &J, const double *(&src)[4], bool &isV) {
-  const int N = a.nG + a.nV;
-  const int64_t v0 = (int64_t)it * a.nV / N, v1 = (int64_t)(it + 1) * a.nV / N;
-  isV = v1 > v0;
-  const int64_t WW = (int64_t)kCyW * kCyW;
-  src[0] = src[1] = src[2] = src[3] = nullptr;
-  if (!isV) {
-    const int i = it - (int)v0;
-    const int c = i % a.ncyc, k = i / a.ncyc;
-    const int32_t *cy = a.cyc + ((int64_t)((a.sg + 1) % a.S) * a.ncyc + c) * 8;
-    const int t1 = cy[0], t2 = cy[1];
-    const int32_t *pa = a.outer + ((int64_t)a.sg * a.T + t1) * 2;
-    const int32_t *pb = a.outer + ((int64_t)a.sg * a.T + t2) * 2;
-    J.blk[0] = pa[0];
-    J.blk[1] = pa[1];
-    J.blk[2] = pb[0];
-    J.blk[3] = pb[1];
-    J.upd[0] = a.rotG[t1] > 0;
-    J.upd[1] = a.rotG[t2] > 0;
-    J.second = false;
-    J.updB[0] = J.updB[1] = false;
-    J.ij[0][0] = J.ij[0][1] = J.ij[1][0] = J.ij[1][1] = 0;
-    J.r0 = (int64_t)k * kCyVSlab;
-    J.r1 = min64(J.r0 + kCyVSlab, a.m);
-    src[0] = a.VpG + t1 * WW;
-    src[1] = a.VpG + t2 * WW;
-    return;
-  }
-  int i = (int)v0, q = 0;
-  if (a.nsrc > 1 && i >= a.ncyc * a.vs[0].nk) {
-    i -= a.ncyc * a.vs[0].nk;
-    q = 1;
-  }
-  const U4Src &v = a.vs[q];
-  const int c = i % a.ncyc, k = v.k0 + (i / a.ncyc) * v.kstep;
-  const int32_t *cy = a.cyc + ((int64_t)((v.sa + 1) % a.S) * a.ncyc + c) * 8;
-  const int t1 = cy[0], t2 = cy[1];
-  const int32_t *pa = a.outer + ((int64_t)v.sa * a.T + t1) * 2;
-  const int32_t *pb = a.outer + ((int64_t)v.sa * a.T + t2) * 2;
-  J.blk[0] = pa[0];
-  J.blk[1] = pa[1];
-  J.blk[2] = pb[0];
-  J.blk[3] = pb[1];
-  J.upd[0] = v.rotA[t1] > 0;
-  J.upd[1] = v.rotA[t2] > 0;
-  J.second = v.second;
-  J.updB[0] = v.second && v.rotB[cy[2]] > 0;
-  J.updB[1] = v.second && v.rotB[cy[3]] > 0;
-  J.ij[0][0] = cy[4];
-  J.ij[0][1] = cy[5];
-  J.ij[1][0] = cy[6];
-  J.ij[1][1] = cy[7];
-  J.r0 = (int64_t)k * kCyVSlab;
-  J.r1 = min64(J.r0 + kCyVSlab, a.nv);
-  src[0] = v.VpA + t1 * WW;
-  src[1] = v.VpA + t2 * WW;
-  if (v.second) {
-    src[2] = v.VpB + cy[2] * WW;
-    src[3] = v.VpB + cy[3] * WW;
-  }
-}
-
-__global__ void __launch_bounds__(kU5Threads, 1) k_update5(U4Args a) {
-  extern __shared__ __align__(128) unsigned char smraw[];
-  U5Smem &S = *reinterpret_cast<U5Smem *>(smraw);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const int N = a.nG + a.nV;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kU5Stages; i++) {
-      mbar_init(&S.full[i], 1);
-      mbar_init(&S.empty[i], 4);
-    }
-    for (int i = 0; i < 2; i++) {
-      mbar_init(&S.pfull[i], 1);
-      mbar_init(&S.pempty[i], 4);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (warp == 0) {
-    // ---- producer: V' + parameters per item, then the item's chunks
-    fence_async_global();
-    unsigned gc = 0;
-    int k = 0;
-    for (int it = blockIdx.x; it < N; it += gridDim.x, k++) {
-      const int slot = k & 1;
-      if (k >= 2) mbar_wait(&S.pempty[slot], ((k >> 1) - 1) & 1);
-      CyV J;
-      const double *src[4];
-      bool isV;
-      u4_item(a, it, J, src, isV);
-      double *A = isV ? a.V : a.G;
-      const int64_t ld = isV ? a.ldv : a.ldg;
-      const bool use[4] = {J.upd[0], J.upd[1], J.updB[0], J.updB[1]};
-      const bool any = use[0] || use[1] || use[2] || use[3];
-      if (!any) J.r1 = J.r0;  // nothing to do: no chunks
-      int nuse = 0;
-      for (int i = 0; i < 4; i++) nuse += use[i];
-      if (lane == 0) {
-        S.prm[slot] = J;
-        S.isv[slot] = isV;
-        for (int b = 0; b < 4; b++) S.gcol[slot][b] = (int64_t)J.blk[b] * 16;
-        mbar_expect_tx(&S.pfull[slot], (uint32_t)nuse * kCyW * kCyW * 8u);
-      }
-      __syncwarp();
-      // V' columns: 32 columns of 256 B per transform (padded stride in smem)
-      for (int i = 0; i < 4; i++)
-        if (use[i]) bulk_g2s(&S.vp[slot][i][lane][0], src[i] + lane * kCyW, kCyW * 8u, &S.pfull[slot]);
-      const int nchunk = (int)cdiv(J.r1 - J.r0, kRch);
-      for (int c = 0; c < nchunk; c++, gc++) {
-        const int st = (int)(gc % kU5Stages);
-        if (gc >= (unsigned)kU5Stages) mbar_wait(&S.empty[st], ((gc / kU5Stages) - 1) & 1);
-        const int64_t r = J.r0 + (int64_t)c * kRch;
-        const uint32_t bytes = (uint32_t)min64(kRch, J.r1 - r) * 8u;
-        if (lane == 0) mbar_expect_tx(&S.full[st], bytes * kCyCols);
-        __syncwarp();
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-          const int j = lane + 32 * h;
-          const int64_t col = (int64_t)J.blk[j >> 4] * 16 + (j & 15);
-          bulk_g2s(&S.ring[st][j][0], A + col * ld + r, bytes, &S.full[st]);
-        }
-      }
-    }
-    return;
-  }
-  // ---- consumers: warp w owns rows 16 (w - 1) .. +16 of every chunk
-  const int cw = warp - 1;
-  unsigned gc = 0;
-  int k = 0;
-  for (int it = blockIdx.x; it < N; it += gridDim.x, k++) {
-    const int slot = k & 1;
-    mbar_wait(&S.pfull[slot], (k >> 1) & 1);
-    const CyV &J = S.prm[slot];
-    const bool isV = S.isv[slot] != 0;
-    double *A = isV ? a.V : a.G;
-    const int64_t ld = isV ? a.ldv : a.ldg;
-    int64_t gcol[4];
-#pragma unroll
-    for (int b = 0; b < 4; b++) gcol[b] = S.gcol[slot][b];
-    unsigned finB = 0;
-    if (J.second) {
-      if (J.updB[0]) finB |= (1u << J.ij[0][0]) | (1u << J.ij[0][1]);
-      if (J.updB[1]) finB |= (1u << J.ij[1][0]) | (1u << J.ij[1][1]);
-    }
-    const unsigned finA = 0xFu & ~finB;
-    const bool keepA = finB != 0;
-    const bool updA0 = J.upd[0], updA1 = J.upd[1], updB0 = J.second && J.updB[0],
-               updB1 = J.second && J.updB[1];
-    const int ib00 = 16 * J.ij[0][0], ib01 = 16 * J.ij[0][1];
-    const int ib10 = 16 * J.ij[1][0], ib11 = 16 * J.ij[1][1];
-    const int64_t r0 = J.r0, r1 = J.r1;
-    const int nchunk = (int)cdiv(r1 - r0, kRch);
-    for (int c = 0; c < nchunk; c++, gc++) {
-      const int st = (int)(gc % kU5Stages);
-      mbar_wait(&S.full[st], (gc / kU5Stages) & 1);
-      double *buf = &S.ring[st][0][0];
-      const int64_t r = r0 + (int64_t)c * kRch;
-      const int nr = (int)min64(kRch, r1 - r);
-      if (updA0)
-        u4_transform(buf, 16 * cw, 0, 16, &S.vp[slot][0][0][0], A, ld, gcol, finA, keepA, r, nr,
-                     g, t);
-      if (updA1)
-        u4_transform(buf, 16 * cw, 32, 48, &S.vp[slot][1][0][0], A, ld, gcol, finA, keepA, r,
-                     nr, g, t);
-      if (updB0 || updB1) __syncwarp();
-      if (updB0)
-        u4_transform(buf, 16 * cw, ib00, ib01, &S.vp[slot][2][0][0], A, ld, gcol, 0xFu, false, r,
-                     nr, g, t);
-      if (updB1)
-        u4_transform(buf, 16 * cw, ib10, ib11, &S.vp[slot][3][0][0], A, ld, gcol, 0xFu, false, r,
-                     nr, g, t);
-      if (keepA) fence_async_smem();  // generic writes before the slot's next TMA fill
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.empty[st]);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&S.pempty[slot]);
-  }
-}
-
-void launch_update5(const U4Args &a, cudaStream_t st) {
-  const size_t smem = sizeof(U5Smem);
-  static int grid = 0;
-  if (!grid) {
-    cudaFuncSetAttribute(k_update5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    grid = sms;
-  }
-  const int N = a.nG + a.nV;
-  k_update5<<<N < grid ? N : grid, kU5Threads, smem, st>>>(a);
-}
-
-void launch_update4(double *G, int64_t ldg, int64_t m, double *V, int64_t ldv, int64_t nv,
-                    const int32_t *outer, const int32_t *plan, int b, int sg, const double *VpG,
-                    const int64_t *rotG, int nsrc, const int *sa, const bool *second,
-                    const double *const *VpA, const int64_t *const *rotA,
-                    const double *const *VpB, const int64_t *const *rotB, const int *k0,
-                    const int *kstep, cudaStream_t st) {
-  U4Args a{};
-  a.G = G;
-  a.ldg = ldg;
-  a.m = m;
-  a.V = V;
-  a.ldv = ldv;
-  a.nv = nv;
-  a.outer = outer;
-  a.cyc = plan;
-  a.S = b - 1;
-  a.T = b / 2;
-  a.ncyc = a.T / 2;
-  a.sg = sg;
-  a.VpG = VpG;
-  a.rotG = rotG;
-  a.nslab_g = sg >= 0 ? (int)cdiv(m, kCyVSlab) : 0;
-  a.nG = a.ncyc * a.nslab_g;
-  const int nslab_v = (int)cdiv(nv, kCyVSlab);
-  a.nsrc = 0;
-  a.nV = 0;
-  for (int q = 0; q < nsrc && V; q++) {
-    U4Src &v = a.vs[a.nsrc];
-    v.sa = sa[q];
-    v.second = second[q];
-    v.VpA = VpA[q];
-    v.VpB = VpB[q] ? VpB[q] : VpA[q];
-    v.rotA = rotA[q];
-    v.rotB = rotB[q] ? rotB[q] : rotA[q];
-    v.k0 = k0[q];
-    v.kstep = kstep[q];
-    v.nk = v.k0 < nslab_v ? (int)cdiv(nslab_v - v.k0, v.kstep) : 0;
-    if (v.nk == 0) continue;
-    a.nV += a.ncyc * v.nk;
-    a.nsrc++;
-  }
-  if (a.nG + a.nV == 0) return;
-  static const int v5 = [] {
-    const char *e = getenv("JHSVD_U4");  // "1": the one-item-per-CTA kernel
-    return !(e && e[0] == '1');
-  }();
-  if (v5) {
-    launch_update5(a, st);
-    return;
-  }
-  const size_t smem = sizeof(CySmem);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_update4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  k_update4<<<a.nG + a.nV, kCyThreads, smem, st>>>(a);
-}
-
 // ---- host side ------------------------------------------------------------------
 
 static long long *g_cy_trace = nullptr;

@@ -53,27 +53,20 @@ int cycle_plan(const int32_t *outer, int b, int32_t *plan);
 bool cycle_ok(int w, int64_t m, int64_t ldg, int64_t nv, int64_t ldv);
 int64_t cycle_workspace_bytes(int64_t n, int w);
 void cycle_trace(void *buf, int64_t cap);
-// one launch: G updates of p-step sg (sg < 0: none) + the V updates of up to
-// two p-step pairs (row slabs k0, k0 + kstep, ...) (jh_cycle.cu)
-void launch_update4(double *G, int64_t ldg, int64_t m, double *V, int64_t ldv, int64_t nv,
-                    const int32_t *outer, const int32_t *plan, int b, int sg, const double *VpG,
-                    const int64_t *rotG, int nsrc, const int *sa, const bool *second,
-                    const double *const *VpA, const int64_t *const *rotA,
-                    const double *const *VpB, const int64_t *const *rotB, const int *k0,
-                    const int *kstep, cudaStream_t st);
-// one launch: G updates of p-step sg (sg < 0: none) + the V updates of up to
-// two p-step pairs (row slabs k0, k0 + kstep, ...) (jh_cycle.cu)
-void launch_update4(double *G, int64_t ldg, int64_t m, double *V, int64_t ldv, int64_t nv,
-                    const int32_t *outer, const int32_t *plan, int b, int sg, const double *VpG,
-                    const int64_t *rotG, int nsrc, const int *sa, const bool *second,
-                    const double *const *VpA, const int64_t *const *rotA,
-                    const double *const *VpB, const int64_t *const *rotB, const int *k0,
-                    const int *kstep, cudaStream_t st);
 // V update of the p-step pair (sa, sa+1) (or sa alone), per cycle and row
-// slab, from the tasks' V' and rotation counts (jh_cycle.cu)
+// slab, from the tasks' V' and rotation counts (jh_vpair.cu)
 void launch_vpair(double *V, int64_t ldv, int64_t nv, const int32_t *outer, const int32_t *plan,
                   int b, int sa, bool second, const double *VpA, const int64_t *rotA,
                   const double *VpB, const int64_t *rotB, cudaStream_t st);
+// one launch: the G update of one p-step (pairs / Vbuf / trot as for
+// launch_update_dmma) and V-pair row slabs of up to two sources (jh_vpair.cu)
+void launch_update_mix(double *G, int64_t ldg, int64_t m, const int32_t *pairs, int ntask,
+                       const double *Vbuf, const int64_t *trot, double *V, int64_t ldv,
+                       int64_t nv, const int32_t *outer, const int32_t *plan, int b, int nsrc,
+                       const int *sa, const bool *second, const double *const *VpA,
+                       const int64_t *const *rotA, const double *const *VpB,
+                       const int64_t *const *rotB, const int *k0, const int *kstep,
+                       cudaStream_t st);
 int launch_cycle(double *G, int64_t ldg, int64_t m, double *V, int64_t ldv, int64_t nv,
                  const int32_t *outer, const int32_t *plan, int b, int s_begin, int nsteps,
                  const int32_t *inner, int64_t n_plus, int inner_limit, double tol_c,

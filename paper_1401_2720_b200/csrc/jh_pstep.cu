@@ -840,17 +840,18 @@ int jh_cycle_trace(void *buf, int64_t cap) {
   return 0;
 }
 
-// Engine 1: the per-p-step Gram and inner kernels, and one update launch
-// per p-step (k_update4, jh_cycle.cu) that post-multiplies the G
-// block-columns of p-step s and -- deferred -- the V block-columns of the
-// previous pair of p-steps (a, a+1): half of the pair's row slabs in the
-// launch of p-step a+1, the other half in that of a+2.  V is read by nothing
-// else during the sweep and every V row still receives the same
-// transformations in the same order, so the results are bitwise those of
-// engine 0; V moves through HBM once per two p-steps instead of once per
-// p-step, and the DMMA-bound V items share the launch with the HBM-bound G
-// items.  The per-task V' and rotation counts of the last four p-steps are
-// kept in a ring.
+// Engine 1 (default for rrow-like tables with V accumulated): the
+// per-p-step Gram and inner Jacobi kernels, then one mixed update launch per
+// p-step: the G update CTAs of p-step s (the per-p-step kernel's) and -- the
+// V update deferred to one pass per pair of p-steps (a, a+1) over the
+// 4-cycles of the pair (jh_vpair.cu) -- half of the pair's V row slabs (the
+// other half in the next launch).  V is read by nothing else during the
+// sweep and every V row still receives the same transformations in the same
+// order, so the results are bitwise those of engine 0; V moves through HBM
+// once per two p-steps, and its DMMA-bound slabs share the SMs with the
+// HBM-bound G slabs.  JHSVD_VPAIR=1 runs the V pass as its own launch after
+// the G update instead.  The per-task V' and rotation counts of the last
+// four p-steps are kept in a ring.
 static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int64_t ldv,
                          int64_t nv, int w, const int32_t *outer, const int32_t *plan,
                          int first_step, int nsteps, const int32_t *inner, int64_t n_plus,
@@ -864,6 +865,10 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
   int64_t *rring = (int64_t *)(Vring + 4 * (int64_t)ntask * ww);
   auto vp = [&](int i) { return Vring + (int64_t)(i % 4) * ntask * ww; };
   auto rt = [&](int i) { return rring + (int64_t)(i % 4) * ntask; };
+  static const bool separate = [] {
+    const char *e = getenv("JHSVD_VPAIR");
+    return e && e[0] == '1';
+  }();
   for (int i = 0; i < nsteps; i++) {
     const int s = first_step + i;
     const int32_t *pairs = outer + (int64_t)s * ntask * 2;
@@ -874,7 +879,23 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
     launch_inner5(Hbuf, vp(i), rt(i), pairs, ntask, w, n_plus, inner, inner_limit, tol_c,
                   counters, s, st);
     prof_mark(st, 1, true);
-    // V work of this launch: up to two (pair, slab set) sources
+    const bool last = (i == nsteps - 1);
+    if (separate) {
+      prof_mark(st, 2, false);
+      launch_update_dmma(G, ldg, m, nullptr, 0, 0, pairs, ntask, w, vp(i), rt(i), st);
+      prof_mark(st, 2, true);
+      g_launches += 3;
+      if (i % 2 == 1 || last) {
+        const bool second = (i % 2 == 1);
+        const int i0 = second ? i - 1 : i;
+        prof_mark(st, 3, false);
+        launch_vpair(V, ldv, nv, outer, plan, b, first_step + i0, second, vp(i0), rt(i0),
+                     second ? vp(i) : nullptr, second ? rt(i) : nullptr, st);
+        prof_mark(st, 3, true);
+        g_launches += 1;
+      }
+      continue;
+    }
     int nsrc = 0, sa[2], k0[2], kstep[2];
     bool second[2];
     const double *VpA[2], *VpB[2];
@@ -890,18 +911,31 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
       kstep[nsrc] = kst;
       nsrc++;
     };
-    const bool last = (i == nsteps - 1);
+    // the V rows of one launch must be disjoint across its sources: a last
+    // p-step without a partner goes to its own launch after the pair's
+    bool tail_single = false;
     if (i % 2 == 1) {
       add(i - 1, true, 0, last ? 1 : 2);  // pair (i-1, i): even slabs now, odd ones next
     } else {
       if (i >= 2) add(i - 2, true, 1, 2);  // odd slabs of pair (i-2, i-1)
-      if (last) add(i, false, 0, 1);       // a last p-step without a partner
+      if (last) {
+        if (nsrc == 0)
+          add(i, false, 0, 1);
+        else
+          tail_single = true;
+      }
     }
     prof_mark(st, 2, false);
-    launch_update4(G, ldg, m, V, ldv, nv, outer, plan, b, s, vp(i), rt(i), nsrc, sa, second, VpA,
-                   rotA, VpB, rotB, k0, kstep, st);
+    launch_update_mix(G, ldg, m, pairs, ntask, vp(i), rt(i), V, ldv, nv, outer, plan, b, nsrc,
+                      sa, second, VpA, rotA, VpB, rotB, k0, kstep, st);
     prof_mark(st, 2, true);
     g_launches += 3;
+    if (tail_single) {
+      prof_mark(st, 3, false);
+      launch_vpair(V, ldv, nv, outer, plan, b, s, false, vp(i), rt(i), nullptr, nullptr, st);
+      prof_mark(st, 3, true);
+      g_launches += 1;
+    }
   }
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : -(int)e;

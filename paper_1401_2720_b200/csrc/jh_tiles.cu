@@ -12,6 +12,7 @@
 // (finite data; such a chain never holds -0.0), so padding is bit-neutral.
 #include "jh_gram.cuh"
 #include "jh_kernels.h"
+#include "jh_update.cuh"
 
 #include <cstdlib>
 
@@ -195,100 +196,6 @@ k_update_dmma(double *__restrict__ G, int64_t ldg, int64_t m, double *__restrict
 // padded ring, V' fragments in registers) and store the results straight to
 // global memory (whole 32 B sectors).  A CTA owns a slab of kUpdSlab rows of
 // one matrix for one task.
-
-constexpr int kUpdStages = 4;
-constexpr int kUpdCons = 4;        // consumer warps
-constexpr int kUpdSlab = 2048;     // rows per CTA
-
-template <int W>
-__global__ void __launch_bounds__(32 * (kUpdCons + 1))
-k_update_tma(double *__restrict__ G, int64_t ldg, int64_t m, double *__restrict__ V,
-             int64_t ldv, int64_t nv, const int32_t *__restrict__ pairs,
-             const double *__restrict__ Vbuf, const int64_t *__restrict__ trot, int nslab_g) {
-  constexpr int NT = W / 8, NK = W / 4, BW = W / 2;
-  extern __shared__ __align__(128) double ring[];  // [kUpdStages][W][kLd]
-  __shared__ __align__(8) uint64_t full[kUpdStages], empty[kUpdStages];
-  const int task = blockIdx.x;
-  if (trot[task] == 0) return;
-  const int p = pairs[2 * task], q = pairs[2 * task + 1];
-  double *A;
-  int64_t ld, rows, s0;
-  if ((int)blockIdx.y < nslab_g) {
-    A = G; ld = ldg; rows = m; s0 = (int64_t)blockIdx.y * kUpdSlab;
-  } else {
-    A = V; ld = ldv; rows = nv; s0 = (int64_t)(blockIdx.y - nslab_g) * kUpdSlab;
-  }
-  const int64_t s1 = min64(s0 + kUpdSlab, rows);
-  const int nchunk = (int)cdiv(s1 - s0, kRch);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kUpdStages; s++) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kUpdCons);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (warp == 0) {
-    // producer
-    for (int c = 0; c < nchunk; c++) {
-      const int s = c % kUpdStages;
-      if (c >= kUpdStages) mbar_wait(&empty[s], (uint32_t)(((c / kUpdStages) - 1) & 1));
-      const int64_t r0 = s0 + (int64_t)c * kRch;
-      const uint32_t bytes = (uint32_t)min64(kRch, s1 - r0) * 8u;
-      if (lane == 0) mbar_expect_tx(&full[s], bytes * W);
-      __syncwarp();
-      for (int j = lane; j < W; j += 32) {
-        const int64_t col = j < BW ? (int64_t)p * BW + j : (int64_t)q * BW + (j - BW);
-        bulk_g2s(ring + ((size_t)s * W + j) * kLd, A + col * ld + r0, bytes, &full[s]);
-      }
-    }
-    return;
-  }
-  // consumers
-  const int cw = warp - 1;
-  const double *Vt = Vbuf + (size_t)task * W * W;
-  double bf[NK][NT];
-#pragma unroll
-  for (int kk = 0; kk < NK; kk++)
-#pragma unroll
-    for (int Y = 0; Y < NT; Y++) bf[kk][Y] = Vt[(8 * Y + g) * W + 4 * kk + t];
-  double *pout = A + ((int64_t)p * BW + 2 * t) * ld;
-  double *qout = A + ((int64_t)q * BW + 2 * t) * ld;
-  for (int c = 0; c < nchunk; c++) {
-    const int s = c % kUpdStages;
-    mbar_wait(&full[s], (uint32_t)((c / kUpdStages) & 1));
-    const int64_t r0 = s0 + (int64_t)c * kRch;
-    const double *buf = ring + (size_t)s * W * kLd;
-#pragma unroll
-    for (int rb = 0; rb < 2; rb++) {
-      const int rl = cw * 16 + rb * 8;
-      double a[NK];
-#pragma unroll
-      for (int kk = 0; kk < NK; kk++) a[kk] = buf[(4 * kk + t) * kLd + rl + g];
-      double acc[NT][2];
-#pragma unroll
-      for (int Y = 0; Y < NT; Y++) acc[Y][0] = acc[Y][1] = 0.0;
-#pragma unroll
-      for (int kk = 0; kk < NK; kk++)
-#pragma unroll
-        for (int Y = 0; Y < NT; Y++) dmma(acc[Y][0], acc[Y][1], a[kk], bf[kk][Y]);
-      const int64_t row = r0 + rl + g;
-      if (row < s1) {
-#pragma unroll
-        for (int Y = 0; Y < NT; Y++)
-#pragma unroll
-          for (int j = 0; j < 2; j++) {
-            double *dst = Y < NT / 2 ? pout + (int64_t)(8 * Y + j) * ld
-                                     : qout + (int64_t)(8 * Y + j - BW) * ld;
-            st_f64(dst + row, acc[Y][j]);
-          }
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-  }
-}
 
 // ---------------------------------------------------------------------------
 // host launchers

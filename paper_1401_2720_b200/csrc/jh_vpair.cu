@@ -1,0 +1,312 @@
+// V update of a pair of p-steps in one pass over V (engine 1).
+//
+// V is read by nothing else until the sweep ends, so the post-multiplication
+// of V by the transforms of p-steps a and a+1 (reference driver.py:165-172,
+// blockkernel.py:407-428) can run as one pass: for the rrow tables, the pairs
+// of two consecutive p-steps form 4-cycles over four block-columns (the
+// cycle plan, jh_cycle.cu), so the 64 V columns of a cycle go through shared
+// memory once, get the two step-a transforms and then the two step-(a+1)
+// transforms, and go back -- V moves through HBM once per two p-steps.
+// Every V row still receives the same transformations in the same order
+// with the same in-order DMMA chains, so the result is bitwise that of two
+// per-p-step updates.
+//
+// CTA = TMA producer warp + 4 DMMA warps, the layout of the per-p-step
+// update kernel (each transform's V' held in registers): warps 1 and 2
+// apply t1 / t2 of p-step a to all 64 rows of a chunk (slot columns 0-31 /
+// 32-63), in place; warps 3 and 4 then apply u1 / u2 of p-step a+1 to their
+// block pairs and store the final values straight from the accumulators.
+// The two phases are pipelined over a 3-stage ring (chunk c's second phase
+// overlaps chunk c+1's first).  Grid: (cycles, row slabs).
+#include "jh_gram.cuh"
+#include "jh_kernels.h"
+#include "jh_update.cuh"
+
+namespace jh {
+
+namespace {
+
+__device__ __forceinline__ void fence_async_smem_cta() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+constexpr int kVW = 32;
+constexpr int kVCols = 64;
+constexpr int kVStages = 3;
+constexpr int kVSlab = 512;  // V rows per CTA (short CTAs: no long tail behind the G slabs)
+
+struct VpSmem {
+  double ring[kVStages][kVCols][kLd];
+  uint64_t full[kVStages], adone[kVStages], empty[kVStages];
+};
+
+struct VpArgs {
+  double *V;
+  int64_t ldv, nv;
+  const int32_t *outer, *cyc;
+  int S, T, ncyc;
+  int sa;
+  bool second;
+  const double *VpA, *VpB;
+  const int64_t *rotA, *rotB;
+};
+
+// rows 0..kRch-1 of the 32 slot columns col(k) = cb0 + k (k < 16),
+// cb1 + k - 16 (k >= 16) times V' (fragments in registers); each result
+// entry goes to the slot in place when keep[block] and to HBM when
+// fin[block] (block = slot block of its column, 0..3)
+__device__ __forceinline__ void vp_transform(double *buf, int cb0, int cb1,
+                                             const double (&bf)[8][4], unsigned keep,
+                                             unsigned fin, double *V, int64_t ldv,
+                                             const int64_t (&gcol)[4], int64_t r, int nr, int g,
+                                             int t) {
+  const int sw = (t >> 1) & 1;  // conflict-free 64-bit shared stores
+#pragma unroll 1
+  for (int rb = 0; rb < kRch / 8; rb += 2) {
+    double a[2][8];
+#pragma unroll
+    for (int h = 0; h < 2; h++)
+#pragma unroll
+      for (int kk = 0; kk < 8; kk++) {
+        const int col = (kk < 4 ? cb0 + 4 * kk : cb1 + 4 * kk - 16) + t;
+        a[h][kk] = buf[col * kLd + 8 * (rb + h) + g];
+      }
+    double acc[2][4][2];
+#pragma unroll
+    for (int h = 0; h < 2; h++)
+#pragma unroll
+      for (int Y = 0; Y < 4; Y++) acc[h][Y][0] = acc[h][Y][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < 8; kk++)
+#pragma unroll
+      for (int h = 0; h < 2; h++)
+#pragma unroll
+        for (int Y = 0; Y < 4; Y++) dmma(acc[h][Y][0], acc[h][Y][1], a[h][kk], bf[kk][Y]);
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int row = 8 * (rb + h) + g;
+#pragma unroll
+      for (int Y = 0; Y < 4; Y++) {
+        const int cbase = Y < 2 ? cb0 : cb1, blk = cbase >> 4;
+        const bool kp = (keep >> blk) & 1, to_g = ((fin >> blk) & 1) && row < nr;
+#pragma unroll
+        for (int jj = 0; jj < 2; jj++) {
+          const int j = jj ^ sw;
+          const double v = j ? acc[h][Y][1] : acc[h][Y][0];
+          const int n = 8 * (Y & 1) + 2 * t + j;
+          if (kp) buf[(cbase + n) * kLd + row] = v;
+          if (to_g) st_f64(V + (gcol[blk] + n) * ldv + r + row, v);
+        }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void vp_load_bfrag(double (&bf)[8][4], const double *Vt, int g, int t) {
+#pragma unroll
+  for (int kk = 0; kk < 8; kk++)
+#pragma unroll
+    for (int Y = 0; Y < 4; Y++) bf[kk][Y] = Vt[(8 * Y + g) * kVW + 4 * kk + t];
+}
+
+// one CTA: cycle c, V row slab k
+__device__ __forceinline__ void vpair_cta(const VpArgs &a, int c, int k, VpSmem &S) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int32_t *cy = a.cyc + ((int64_t)((a.sa + 1) % a.S) * a.ncyc + c) * 8;
+  const int tk[2] = {cy[0], cy[1]}, uk[2] = {cy[2], cy[3]};
+  const int32_t *pa = a.outer + ((int64_t)a.sa * a.T + tk[0]) * 2;
+  const int32_t *pb = a.outer + ((int64_t)a.sa * a.T + tk[1]) * 2;
+  int64_t gcol[4] = {(int64_t)pa[0] * 16, (int64_t)pa[1] * 16, (int64_t)pb[0] * 16,
+                     (int64_t)pb[1] * 16};
+  const bool updA[2] = {a.rotA[tk[0]] > 0, a.rotA[tk[1]] > 0};
+  const bool updB[2] = {a.second && a.rotB[uk[0]] > 0, a.second && a.rotB[uk[1]] > 0};
+  if (!(updA[0] || updA[1] || updB[0] || updB[1])) return;
+  const int ib[2][2] = {{cy[4], cy[5]}, {cy[6], cy[7]}};
+  // blocks a transform B rewrites: their transform-A values stay in the slot
+  unsigned touchedB = 0;
+  for (int h = 0; h < 2; h++)
+    if (updB[h]) touchedB |= (1u << ib[h][0]) | (1u << ib[h][1]);
+  const int64_t r0 = (int64_t)k * kVSlab, r1 = min64(r0 + kVSlab, a.nv);
+  const int nchunk = (int)cdiv(r1 - r0, kRch);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kVStages; i++) {
+      mbar_init(&S.full[i], 1);
+      mbar_init(&S.adone[i], 2);
+      mbar_init(&S.empty[i], 2);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == 0) {
+    for (int cc = 0; cc < nchunk; cc++) {
+      const int st = cc % kVStages;
+      if (cc >= kVStages) mbar_wait(&S.empty[st], (uint32_t)(((cc / kVStages) - 1) & 1));
+      const int64_t r = r0 + (int64_t)cc * kRch;
+      const uint32_t bytes = (uint32_t)min64(kRch, r1 - r) * 8u;
+      if (lane == 0) mbar_expect_tx(&S.full[st], bytes * kVCols);
+      __syncwarp();
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int j = lane + 32 * h;
+        bulk_g2s(&S.ring[st][j][0], a.V + (gcol[j >> 4] + (j & 15)) * a.ldv + r, bytes,
+                 &S.full[st]);
+      }
+    }
+    return;
+  }
+  const int role = warp - 1;  // 0, 1: transform A of t1 / t2; 2, 3: transform B of u1 / u2
+  const int h = role & 1;
+  const bool phaseA = role < 2;
+  const bool mine = phaseA ? updA[h] : updB[h];
+  double bf[8][4];
+  if (mine) vp_load_bfrag(bf, (phaseA ? a.VpA + (int64_t)tk[h] * kVW * kVW
+                                      : a.VpB + (int64_t)uk[h] * kVW * kVW), g, t);
+  const int cb0 = phaseA ? 32 * h : 16 * ib[h][0];
+  const int cb1 = phaseA ? 32 * h + 16 : 16 * ib[h][1];
+  const unsigned keep = phaseA ? touchedB : 0u;
+  const unsigned fin = phaseA ? (0xFu & ~touchedB) : 0xFu;
+  for (int cc = 0; cc < nchunk; cc++) {
+    const int st = cc % kVStages;
+    const uint32_t par = (uint32_t)((cc / kVStages) & 1);
+    mbar_wait(phaseA ? &S.full[st] : &S.adone[st], par);
+    double *buf = &S.ring[st][0][0];
+    const int64_t r = r0 + (int64_t)cc * kRch;
+    const int nr = (int)min64(kRch, r1 - r);
+    if (mine) vp_transform(buf, cb0, cb1, bf, keep, fin, a.V, a.ldv, gcol, r, nr, g, t);
+    if (phaseA && mine && keep) fence_async_smem_cta();  // before the slot's next TMA fill
+    __syncwarp();
+    if (lane == 0) mbar_arrive(phaseA ? &S.adone[st] : &S.empty[st]);
+  }
+}
+
+__global__ void __launch_bounds__(160, 2) k_vpair(VpArgs a) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  vpair_cta(a, blockIdx.x, blockIdx.y, *reinterpret_cast<VpSmem *>(smraw));
+}
+
+// ---- one launch: the G update of p-step s (per-task CTAs of the per-p-step
+// kernel) and V-pair row slabs (vpair_cta), interleaved over the grid so
+// that HBM-bound G slabs and DMMA-bound V slabs share the SMs
+
+struct MixArgs {
+  double *G;
+  int64_t ldg, m;
+  const int32_t *pairs;
+  const double *Vbuf;
+  const int64_t *trot;
+  int ntask, nslab_g, nG;
+  VpArgs vp[2];
+  int k0[2], kstep[2], nk[2];
+  int nsrc, nV;
+};
+
+union MixSmem {
+  struct {
+    double ring[kUpdStages][kVW][kLd];
+    uint64_t full[kUpdStages], empty[kUpdStages];
+  } g;
+  VpSmem v;
+};
+
+__global__ void __launch_bounds__(160, 2) k_update_mix(MixArgs a) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  MixSmem &S = *reinterpret_cast<MixSmem *>(smraw);
+  const int N = a.nG + a.nV, bid = blockIdx.x;
+  const int64_t v0 = (int64_t)bid * a.nV / N, v1 = (int64_t)(bid + 1) * a.nV / N;
+  if (v1 == v0) {
+    const int i = bid - (int)v0;
+    update_tma_cta<kVW>(a.G, a.ldg, a.m, nullptr, 0, 0, a.pairs, a.Vbuf, a.trot, a.nslab_g,
+                        i % a.ntask, i / a.ntask, &S.g.ring[0][0][0], S.g.full, S.g.empty);
+    return;
+  }
+  int i = (int)v0, q = 0;
+  const int ncyc = a.vp[0].ncyc;
+  if (a.nsrc > 1 && i >= ncyc * a.nk[0]) {
+    i -= ncyc * a.nk[0];
+    q = 1;
+  }
+  vpair_cta(a.vp[q], i % ncyc, a.k0[q] + (i / ncyc) * a.kstep[q], S.v);
+}
+
+}  // namespace
+
+void launch_vpair(double *V, int64_t ldv, int64_t nv, const int32_t *outer, const int32_t *plan,
+                  int b, int sa, bool second, const double *VpA, const int64_t *rotA,
+                  const double *VpB, const int64_t *rotB, cudaStream_t st) {
+  VpArgs a{};
+  a.V = V;
+  a.ldv = ldv;
+  a.nv = nv;
+  a.outer = outer;
+  a.cyc = plan;
+  a.S = b - 1;
+  a.T = b / 2;
+  a.ncyc = a.T / 2;
+  a.sa = sa;
+  a.second = second;
+  a.VpA = VpA;
+  a.VpB = VpB ? VpB : VpA;
+  a.rotA = rotA;
+  a.rotB = rotB ? rotB : rotA;
+  const size_t smem = sizeof(VpSmem);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_vpair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  dim3 grid(a.ncyc, (unsigned)cdiv(nv, kVSlab));
+  k_vpair<<<grid, 160, smem, st>>>(a);
+}
+
+void launch_update_mix(double *G, int64_t ldg, int64_t m, const int32_t *pairs, int ntask,
+                       const double *Vbuf, const int64_t *trot, double *V, int64_t ldv,
+                       int64_t nv, const int32_t *outer, const int32_t *plan, int b, int nsrc,
+                       const int *sa, const bool *second, const double *const *VpA,
+                       const int64_t *const *rotA, const double *const *VpB,
+                       const int64_t *const *rotB, const int *k0, const int *kstep,
+                       cudaStream_t st) {
+  MixArgs a{};
+  a.G = G;
+  a.ldg = ldg;
+  a.m = m;
+  a.pairs = pairs;
+  a.Vbuf = Vbuf;
+  a.trot = trot;
+  a.ntask = ntask;
+  a.nslab_g = (int)cdiv(m, kUpdSlab);
+  a.nG = ntask * a.nslab_g;
+  const int nslab_v = (int)cdiv(nv, kVSlab);
+  for (int q = 0; q < nsrc && V; q++) {
+    VpArgs &v = a.vp[a.nsrc];
+    v.V = V;
+    v.ldv = ldv;
+    v.nv = nv;
+    v.outer = outer;
+    v.cyc = plan;
+    v.S = b - 1;
+    v.T = b / 2;
+    v.ncyc = v.T / 2;
+    v.sa = sa[q];
+    v.second = second[q];
+    v.VpA = VpA[q];
+    v.VpB = VpB[q] ? VpB[q] : VpA[q];
+    v.rotA = rotA[q];
+    v.rotB = rotB[q] ? rotB[q] : rotA[q];
+    a.k0[a.nsrc] = k0[q];
+    a.kstep[a.nsrc] = kstep[q];
+    a.nk[a.nsrc] = k0[q] < nslab_v ? (int)cdiv(nslab_v - k0[q], kstep[q]) : 0;
+    if (a.nk[a.nsrc] == 0) continue;
+    a.nV += v.ncyc * a.nk[a.nsrc];
+    a.nsrc++;
+  }
+  if (a.nG + a.nV == 0) return;
+  const size_t smem = sizeof(MixSmem);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_update_mix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_update_mix<<<a.nG + a.nV, 160, smem, st>>>(a);
+}
+
+}  // namespace jh

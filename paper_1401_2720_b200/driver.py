@@ -107,11 +107,12 @@ class SweepEngine:
                  outer: PStrategy, inner: PStrategy, n_plus: int,
                  engine: Optional[int] = None):
         """``engine`` (all bitwise equal, see jh_block_sweep2): 0 per-p-step
-        kernels (default; fastest measured), 1 per-p-step kernels with the V
-        update paired over two p-steps, 2 the cycle engine.  Engines 1 and
-        2 need an outer table that pairs block-columns in 4-cycles (rrow);
-        JHSVD_ENGINE selects the default.  profiles/r01/cycle_engine.md has
-        the measurements."""
+        kernels, 1 per-p-step Gram / inner kernels with the V update paired
+        over two p-steps and mixed into the G update launch (default when V
+        is accumulated and the outer table pairs block-columns in 4-cycles,
+        e.g. rrow; falls back to 0 otherwise), 2 the cycle engine (opt-in).
+        JHSVD_ENGINE overrides.  profiles/r01/cycle_engine.md has the
+        measurements."""
         import os
 
         import torch
@@ -135,7 +136,7 @@ class SweepEngine:
         self.nsteps = outer.num_steps
         if engine is None:
             env = os.environ.get("JHSVD_ENGINE")
-            engine = int(env) if env else 0
+            engine = int(env) if env else (1 if nv > 0 else 0)
         self.plan_dev = self._cycle_plan(outer) if engine in (1, 2) else None
         self.engine = engine if self.plan_dev is not None else 0
         nbytes = int(self.lib.jh_sweep_workspace_bytes(n, w))

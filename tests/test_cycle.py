@@ -93,6 +93,8 @@ def _graded(m, n, seed, kappa=1e6):
     (512, 512, 0, None, True, 256),     # hyperbolic (J signature)
     (4096, 256, 0, None, True, 256),    # long rows: many chunks per item
     (2050, 512, 0, None, True, 512),    # m not a multiple of the chunk
+    (1024, 1024, 0, None, True, 1024),  # V in two row slabs, odd p-step count
+    (4096, 4096, 0, 9, True, 4096),     # many V slabs, odd count
 ])
 def test_engine_sweep_bitwise_vs_pstep_kernels(m, n, first, count, with_v, n_plus, engine):
     import torch
