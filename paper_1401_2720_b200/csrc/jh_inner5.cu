@@ -14,13 +14,24 @@ __global__ void __launch_bounds__(InnerCfg5<W>::NTH)
 k_factor_inner5(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
                 int64_t *__restrict__ task_rot, const int32_t *__restrict__ pairs,
                 int64_t n_plus, const int32_t *__restrict__ inner, int inner_limit,
-                double tol_c, unsigned long long *counters, int pstep, bool from_r) {
+                double tol_c, unsigned long long *counters, int pstep, bool from_r,
+                int64_t *done, int64_t epoch) {
   extern __shared__ __align__(16) unsigned char smraw[];
+  // a programmatically dependent launch (the engine-1 update) may start now:
+  // it waits for each task's `done` flag instead of for this whole grid
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int task = blockIdx.x;
   inner5_task<W, InnerCfg5<W>::NTH>(smraw, Hbuf + (size_t)task * W * W, Vbuf + (size_t)task * W * W,
                                     pairs[2 * task], pairs[2 * task + 1], n_plus, inner,
                                     inner_limit, tol_c, counters, pstep, task, &task_rot[task],
                                     from_r);
+  if (done) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(done + task), "l"(epoch) : "memory");
+    }
+  }
 }
 
 bool inner5_ok(int w) { return w == 16 || w == 32 || w == 64; }
@@ -29,7 +40,7 @@ template <int W>
 static void launch_inner5_t(const double *Hbuf, double *Vbuf, int64_t *trot, const int32_t *pairs,
                            int ntask, int64_t n_plus, const int32_t *inner, int inner_limit,
                            double tol_c, unsigned long long *counters, int pstep,
-                           cudaStream_t st, bool from_r) {
+                           cudaStream_t st, bool from_r, int64_t *done, int64_t epoch) {
   const size_t smem = sizeof(InnerSmem5<W>);
   static bool attr = false;
   if (!attr) {
@@ -39,22 +50,22 @@ static void launch_inner5_t(const double *Hbuf, double *Vbuf, int64_t *trot, con
   }
   k_factor_inner5<W><<<ntask, InnerCfg5<W>::NTH, smem, st>>>(Hbuf, Vbuf, trot, pairs, n_plus, inner,
                                                            inner_limit, tol_c, counters, pstep,
-                                                           from_r);
+                                                           from_r, done, epoch);
 }
 
 void launch_inner5(const double *Hbuf, double *Vbuf, int64_t *trot, const int32_t *pairs,
                    int ntask, int w, int64_t n_plus, const int32_t *inner, int inner_limit,
                    double tol_c, unsigned long long *counters, int pstep, cudaStream_t st,
-                   bool from_r) {
+                   bool from_r, int64_t *done, int64_t epoch) {
   if (w == 16)
     launch_inner5_t<16>(Hbuf, Vbuf, trot, pairs, ntask, n_plus, inner, inner_limit, tol_c,
-                       counters, pstep, st, from_r);
+                       counters, pstep, st, from_r, done, epoch);
   else if (w == 32)
     launch_inner5_t<32>(Hbuf, Vbuf, trot, pairs, ntask, n_plus, inner, inner_limit, tol_c,
-                       counters, pstep, st, from_r);
+                       counters, pstep, st, from_r, done, epoch);
   else
     launch_inner5_t<64>(Hbuf, Vbuf, trot, pairs, ntask, n_plus, inner, inner_limit, tol_c,
-                       counters, pstep, st, from_r);
+                       counters, pstep, st, from_r, done, epoch);
 }
 
 }  // namespace jh

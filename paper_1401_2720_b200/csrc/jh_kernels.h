@@ -34,10 +34,11 @@ void launch_inner4(const double *Hbuf, double *Vbuf, int64_t *trot, const int32_
 // the first v3 inner Jacobi, kept for A/B timing (jh_inner5.cu)
 bool inner5_ok(int w);
 // from_r: Hbuf holds the shortened factors R (QR peel-off) instead of Grams
+// done (optional): done[task] = epoch (release) once the task's V' is written
 void launch_inner5(const double *Hbuf, double *Vbuf, int64_t *trot, const int32_t *pairs,
                    int ntask, int w, int64_t n_plus, const int32_t *inner, int inner_limit,
                    double tol_c, unsigned long long *counters, int pstep, cudaStream_t st,
-                   bool from_r = false);
+                   bool from_r = false, int64_t *done = nullptr, int64_t epoch = 0);
 
 // QR peel-off shortening of every task of a p-step (jh_qr.cu): Rbuf[task] =
 // R (w x w, column-major) of the pair [Gp Gq]; w even <= 32, m % w == 0
@@ -66,7 +67,8 @@ void launch_update_mix(double *G, int64_t ldg, int64_t m, const int32_t *pairs, 
                        const int *sa, const bool *second, const double *const *VpA,
                        const int64_t *const *rotA, const double *const *VpB,
                        const int64_t *const *rotB, const int *k0, const int *kstep,
-                       cudaStream_t st);
+                       cudaStream_t st, const int64_t *done = nullptr, int64_t epoch = 0,
+                       int cur_step = -1);
 int launch_cycle(double *G, int64_t ldg, int64_t m, double *V, int64_t ldv, int64_t nv,
                  const int32_t *outer, const int32_t *plan, int b, int s_begin, int nsteps,
                  const int32_t *inner, int64_t n_plus, int inner_limit, double tol_c,

@@ -704,7 +704,8 @@ int jh_profile_end(double *ms, int64_t *count) {
 // the cycle engine's own area (engine 2 only).
 static int64_t ws_base_bytes(int64_t n, int w) {
   const int64_t ntask = n / w;  // b/2 with b = n / (w/2)
-  return ntask * (int64_t)w * w * 8 * 5 + ntask * 8 * 4 + 256;
+  // H | V' ring (4) | rotation-count ring (4) | per-task done flags (engine 1)
+  return ntask * (int64_t)w * w * 8 * 5 + ntask * 8 * 4 + ntask * 8 + 256;
 }
 
 // Bytes of device workspace jh_block_sweep (engines 0 and 1) needs.
@@ -863,22 +864,35 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
   double *Hbuf = (double *)workspace;
   double *Vring = Hbuf + (int64_t)ntask * ww;
   int64_t *rring = (int64_t *)(Vring + 4 * (int64_t)ntask * ww);
+  int64_t *done = rring + 4 * (int64_t)ntask;
   auto vp = [&](int i) { return Vring + (int64_t)(i % 4) * ntask * ww; };
   auto rt = [&](int i) { return rring + (int64_t)(i % 4) * ntask; };
   static const bool separate = [] {
     const char *e = getenv("JHSVD_VPAIR");
     return e && e[0] == '1';
   }();
+  // overlap of the inner Jacobi's tail with the update (programmatic
+  // dependent launch + per-task flags); JHSVD_PDL=0 disables
+  static const bool pdl = [] {
+    const char *e = getenv("JHSVD_PDL");
+    return !(e && e[0] == '0');
+  }();
+  static int64_t epoch = 0;
+  if (pdl && !separate) cudaMemsetAsync(done, 0xff, sizeof(int64_t) * ntask, st);
   for (int i = 0; i < nsteps; i++) {
     const int s = first_step + i;
     const int32_t *pairs = outer + (int64_t)s * ntask * 2;
     prof_mark(st, 0, false);
     launch_gram_tma(G, ldg, m, pairs, ntask, w, Hbuf, st);
     prof_mark(st, 0, true);
+    const bool use_pdl = pdl && !separate;
+    if (use_pdl) epoch++;
+    // (with the programmatic launch, class 1 times the inner Jacobi and the
+    // overlapped update together)
     prof_mark(st, 1, false);
     launch_inner5(Hbuf, vp(i), rt(i), pairs, ntask, w, n_plus, inner, inner_limit, tol_c,
-                  counters, s, st);
-    prof_mark(st, 1, true);
+                  counters, s, st, false, use_pdl ? done : nullptr, epoch);
+    if (!use_pdl) prof_mark(st, 1, true);
     const bool last = (i == nsteps - 1);
     if (separate) {
       prof_mark(st, 2, false);
@@ -925,10 +939,11 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
           tail_single = true;
       }
     }
-    prof_mark(st, 2, false);
+    if (!use_pdl) prof_mark(st, 2, false);
     launch_update_mix(G, ldg, m, pairs, ntask, vp(i), rt(i), V, ldv, nv, outer, plan, b, nsrc,
-                      sa, second, VpA, rotA, VpB, rotB, k0, kstep, st);
-    prof_mark(st, 2, true);
+                      sa, second, VpA, rotA, VpB, rotB, k0, kstep, st, use_pdl ? done : nullptr,
+                      epoch, s);
+    prof_mark(st, use_pdl ? 1 : 2, true);
     g_launches += 3;
     if (tail_single) {
       prof_mark(st, 3, false);

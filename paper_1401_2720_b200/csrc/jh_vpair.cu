@@ -30,6 +30,19 @@ __device__ __forceinline__ void fence_async_smem_cta() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// thread 0 spins until flag == epoch (acquire), then the CTA proceeds
+__device__ __forceinline__ void wait_flag_cta(const int64_t *flag, int64_t epoch) {
+  if (threadIdx.x == 0) {
+    for (;;) {
+      int64_t v;
+      asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+      if (v == epoch) break;
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+}
+
 constexpr int kVW = 32;
 constexpr int kVCols = 64;
 constexpr int kVStages = 3;
@@ -49,6 +62,9 @@ struct VpArgs {
   bool second;
   const double *VpA, *VpB;
   const int64_t *rotA, *rotB;
+  const int64_t *doneA;  // non-null: the step-a tasks may still be running
+  const int64_t *doneB;  // non-null: the step-(a+1) tasks may still be running
+  int64_t epoch;
 };
 
 // rows 0..kRch-1 of the 32 slot columns col(k) = cb0 + k (k < 16),
@@ -114,6 +130,14 @@ __device__ __forceinline__ void vpair_cta(const VpArgs &a, int c, int k, VpSmem 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int32_t *cy = a.cyc + ((int64_t)((a.sa + 1) % a.S) * a.ncyc + c) * 8;
   const int tk[2] = {cy[0], cy[1]}, uk[2] = {cy[2], cy[3]};
+  if (a.doneA) {
+    wait_flag_cta(a.doneA + tk[0], a.epoch);
+    wait_flag_cta(a.doneA + tk[1], a.epoch);
+  }
+  if (a.second && a.doneB) {
+    wait_flag_cta(a.doneB + uk[0], a.epoch);
+    wait_flag_cta(a.doneB + uk[1], a.epoch);
+  }
   const int32_t *pa = a.outer + ((int64_t)a.sa * a.T + tk[0]) * 2;
   const int32_t *pb = a.outer + ((int64_t)a.sa * a.T + tk[1]) * 2;
   int64_t gcol[4] = {(int64_t)pa[0] * 16, (int64_t)pa[1] * 16, (int64_t)pb[0] * 16,
@@ -194,6 +218,8 @@ struct MixArgs {
   const int32_t *pairs;
   const double *Vbuf;
   const int64_t *trot;
+  const int64_t *done;  // non-null: launched programmatically after the inner kernel
+  int64_t epoch;
   int ntask, nslab_g, nG;
   VpArgs vp[2];
   int k0[2], kstep[2], nk[2];
@@ -215,6 +241,7 @@ __global__ void __launch_bounds__(160, 2) k_update_mix(MixArgs a) {
   const int64_t v0 = (int64_t)bid * a.nV / N, v1 = (int64_t)(bid + 1) * a.nV / N;
   if (v1 == v0) {
     const int i = bid - (int)v0;
+    if (a.done) wait_flag_cta(a.done + i % a.ntask, a.epoch);
     update_tma_cta<kVW>(a.G, a.ldg, a.m, nullptr, 0, 0, a.pairs, a.Vbuf, a.trot, a.nslab_g,
                         i % a.ntask, i / a.ntask, &S.g.ring[0][0][0], S.g.full, S.g.empty);
     return;
@@ -234,6 +261,7 @@ void launch_vpair(double *V, int64_t ldv, int64_t nv, const int32_t *outer, cons
                   int b, int sa, bool second, const double *VpA, const int64_t *rotA,
                   const double *VpB, const int64_t *rotB, cudaStream_t st) {
   VpArgs a{};
+  a.doneA = a.doneB = nullptr;
   a.V = V;
   a.ldv = ldv;
   a.nv = nv;
@@ -264,8 +292,10 @@ void launch_update_mix(double *G, int64_t ldg, int64_t m, const int32_t *pairs, 
                        const int *sa, const bool *second, const double *const *VpA,
                        const int64_t *const *rotA, const double *const *VpB,
                        const int64_t *const *rotB, const int *k0, const int *kstep,
-                       cudaStream_t st) {
+                       cudaStream_t st, const int64_t *done, int64_t epoch, int cur_step) {
   MixArgs a{};
+  a.done = done;
+  a.epoch = epoch;
   a.G = G;
   a.ldg = ldg;
   a.m = m;
@@ -292,6 +322,9 @@ void launch_update_mix(double *G, int64_t ldg, int64_t m, const int32_t *pairs, 
     v.VpB = VpB[q] ? VpB[q] : VpA[q];
     v.rotA = rotA[q];
     v.rotB = rotB[q] ? rotB[q] : rotA[q];
+    v.doneA = (done && sa[q] == cur_step) ? done : nullptr;
+    v.doneB = (done && second[q] && sa[q] + 1 == cur_step) ? done : nullptr;
+    v.epoch = epoch;
     a.k0[a.nsrc] = k0[q];
     a.kstep[a.nsrc] = kstep[q];
     a.nk[a.nsrc] = k0[q] < nslab_v ? (int)cdiv(nslab_v - k0[q], kstep[q]) : 0;
@@ -306,7 +339,22 @@ void launch_update_mix(double *G, int64_t ldg, int64_t m, const int32_t *pairs, 
     cudaFuncSetAttribute(k_update_mix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_update_mix<<<a.nG + a.nV, 160, smem, st>>>(a);
+  if (!done) {
+    k_update_mix<<<a.nG + a.nV, 160, smem, st>>>(a);
+    return;
+  }
+  // programmatic dependent launch: may start while the inner kernel runs
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = dim3(a.nG + a.nV);
+  cfg.blockDim = dim3(160);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = pdl;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_update_mix, a);
 }
 
 }  // namespace jh
