@@ -81,6 +81,11 @@ int jh_block_sweep2(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int
                     int64_t n_plus, int inner_limit, double tol_c, void *workspace,
                     int64_t ws_bytes, unsigned long long *counters, void *stream);
 
+/* Engine 1: 1 (default) lets the update launch start while the inner Jacobi
+ * kernel still runs (programmatic dependent launch, per-task flags); 0 keeps
+ * the kernels apart (per-kernel timing).  Results are identical. */
+int jh_set_overlap(int on);
+
 /* Diagnostic: per-work-item trace of the cycle engine, records {item,
  * smid, start ns, end ns} (int64) into device buf[4 + 4 cap], buf[0] =
  * count; NULL disables. */

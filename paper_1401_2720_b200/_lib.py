@@ -36,6 +36,7 @@ SIGNATURES = {
                                  _c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_i64,
                                  _c_i32, _c_d, _c_p, _c_i64, _c_p, _c_p]),
     "jh_cycle_trace": (_c_i32, [_c_p, _c_i64]),
+    "jh_set_overlap": (_c_i32, [_c_i32]),
     "jh_gram": (_c_i32, [_c_p, _c_i64, _c_i64, _c_i32, _c_p, _c_p]),
     "jh_qr_peeloff": (_c_i32, [_c_p, _c_i64, _c_i64, _c_i32, _c_p, _c_p]),
     "jh_cholesky": (_c_i32, [_c_p, _c_i32, _c_p, _c_p, _c_p]),

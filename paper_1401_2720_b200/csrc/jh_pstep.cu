@@ -639,6 +639,11 @@ struct Profiler {
   int *cls = nullptr;
 };
 static Profiler g_prof;
+// engine 1: overlap the update launch with the inner kernel (jh_set_overlap)
+static bool g_overlap = [] {
+  const char *e = getenv("JHSVD_PDL");
+  return !(e && e[0] == '0');
+}();
 unsigned long long g_launches = 0;
 
 static inline void prof_mark(cudaStream_t st, int cls, bool after) {
@@ -833,6 +838,13 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
   return e == cudaSuccess ? 0 : -(int)e;
 }
 
+// Engine 1: overlap the update launch with the inner Jacobi's tail (1,
+// default) or keep every kernel apart (0, for per-kernel timing).
+int jh_set_overlap(int on) {
+  g_overlap = on != 0;
+  return 0;
+}
+
 // Diagnostic: record one {item, smid, start ns, end ns} int64 record per
 // cycle-engine work item into buf (device, int64[4 + 4 cap]; buf[0] = count)
 // on subsequent launches; buf = NULL disables.
@@ -872,11 +884,9 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
     return e && e[0] == '1';
   }();
   // overlap of the inner Jacobi's tail with the update (programmatic
-  // dependent launch + per-task flags); JHSVD_PDL=0 disables
-  static const bool pdl = [] {
-    const char *e = getenv("JHSVD_PDL");
-    return !(e && e[0] == '0');
-  }();
+  // dependent launch + per-task flags); JHSVD_PDL=0 or jh_set_overlap(0)
+  // disables (per-kernel timing needs the kernels apart)
+  const bool pdl = g_overlap;
   static int64_t epoch = 0;
   if (pdl && !separate) cudaMemsetAsync(done, 0xff, sizeof(int64_t) * ntask, st);
   for (int i = 0; i < nsteps; i++) {
