@@ -68,7 +68,11 @@ void launch_update_mix(double *G, int64_t ldg, int64_t m, const int32_t *pairs, 
                        const int64_t *const *rotA, const double *const *VpB,
                        const int64_t *const *rotB, const int *k0, const int *kstep,
                        cudaStream_t st, const int64_t *done = nullptr, int64_t epoch = 0,
-                       int cur_step = -1);
+                       int cur_step = -1, double *Hnext = nullptr, double *gstate = nullptr,
+                       int64_t *sflag = nullptr);
+// Hnext != null: the G items also form the Gram matrices of p-step
+// cur_step + 1 into Hnext (gstate: cycles x 2 x 640 doubles of chain state,
+// sflag: cycles int64, both scratch)
 int launch_cycle(double *G, int64_t ldg, int64_t m, double *V, int64_t ldv, int64_t nv,
                  const int32_t *outer, const int32_t *plan, int b, int s_begin, int nsteps,
                  const int32_t *inner, int64_t n_plus, int inner_limit, double tol_c,

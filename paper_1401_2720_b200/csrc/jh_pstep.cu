@@ -710,7 +710,10 @@ int jh_profile_end(double *ms, int64_t *count) {
 static int64_t ws_base_bytes(int64_t n, int w) {
   const int64_t ntask = n / w;  // b/2 with b = n / (w/2)
   // H | V' ring (4) | rotation-count ring (4) | per-task done flags (engine 1)
-  return ntask * (int64_t)w * w * 8 * 5 + ntask * 8 * 4 + ntask * 8 + 256;
+  // | second H, Gram chain states, per-cycle slab flags (engine 1, fused Gram)
+  const int64_t ncyc = ntask / 2 > 0 ? ntask / 2 : 1;
+  return ntask * (int64_t)w * w * 8 * 5 + ntask * 8 * 4 + ntask * 8 + ntask * (int64_t)w * w * 8 +
+         ncyc * 2 * 640 * 8 + ncyc * 8 + 1024;
 }
 
 // Bytes of device workspace jh_block_sweep (engines 0 and 1) needs.
@@ -877,6 +880,10 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
   double *Vring = Hbuf + (int64_t)ntask * ww;
   int64_t *rring = (int64_t *)(Vring + 4 * (int64_t)ntask * ww);
   int64_t *done = rring + 4 * (int64_t)ntask;
+  double *Hbuf2 = (double *)(done + ntask);
+  double *gstate = Hbuf2 + (int64_t)ntask * ww;
+  int64_t *sflag = (int64_t *)(gstate + (int64_t)(ntask / 2) * 2 * 640);
+  auto hb = [&](int i) { return (i % 2) ? Hbuf2 : Hbuf; };
   auto vp = [&](int i) { return Vring + (int64_t)(i % 4) * ntask * ww; };
   auto rt = [&](int i) { return rring + (int64_t)(i % 4) * ntask; };
   static const bool separate = [] {
@@ -889,18 +896,31 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
   const bool pdl = g_overlap;
   static int64_t epoch = 0;
   if (pdl && !separate) cudaMemsetAsync(done, 0xff, sizeof(int64_t) * ntask, st);
+  // opt-in (JHSVD_GU=1): the update launch of p-step s also forms the
+  // Grams of p-step s+1 (one pass over G per p-step, Gram chains handed
+  // from row slab to row slab); bitwise equal but slower on B200 (the
+  // chain hand-offs serialise the slabs of a cycle: 2.33 vs 2.06 ms per
+  // p-step at n = 16384, profiles/r01/cycle_engine.md)
+  static const bool fuse_gram = [] {
+    const char *e = getenv("JHSVD_GU");
+    return e && e[0] == '1';
+  }();
+  const bool gu = fuse_gram && !separate && w == 32;
+  if (gu) cudaMemsetAsync(sflag, 0xff, sizeof(int64_t) * (ntask / 2), st);
   for (int i = 0; i < nsteps; i++) {
     const int s = first_step + i;
     const int32_t *pairs = outer + (int64_t)s * ntask * 2;
-    prof_mark(st, 0, false);
-    launch_gram_tma(G, ldg, m, pairs, ntask, w, Hbuf, st);
-    prof_mark(st, 0, true);
+    if (!gu || i == 0) {
+      prof_mark(st, 0, false);
+      launch_gram_tma(G, ldg, m, pairs, ntask, w, hb(i), st);
+      prof_mark(st, 0, true);
+    }
     const bool use_pdl = pdl && !separate;
     if (use_pdl) epoch++;
     // (with the programmatic launch, class 1 times the inner Jacobi and the
     // overlapped update together)
     prof_mark(st, 1, false);
-    launch_inner5(Hbuf, vp(i), rt(i), pairs, ntask, w, n_plus, inner, inner_limit, tol_c,
+    launch_inner5(hb(i), vp(i), rt(i), pairs, ntask, w, n_plus, inner, inner_limit, tol_c,
                   counters, s, st, false, use_pdl ? done : nullptr, epoch);
     if (!use_pdl) prof_mark(st, 1, true);
     const bool last = (i == nsteps - 1);
@@ -950,9 +970,10 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
       }
     }
     if (!use_pdl) prof_mark(st, 2, false);
+    const bool gu_now = gu && !last;
     launch_update_mix(G, ldg, m, pairs, ntask, vp(i), rt(i), V, ldv, nv, outer, plan, b, nsrc,
                       sa, second, VpA, rotA, VpB, rotB, k0, kstep, st, use_pdl ? done : nullptr,
-                      epoch, s);
+                      epoch, s, gu_now ? hb(i + 1) : nullptr, gstate, sflag);
     prof_mark(st, use_pdl ? 1 : 2, true);
     g_launches += 3;
     if (tail_single) {
