@@ -26,10 +26,17 @@ k_factor_inner5(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
                                     inner_limit, tol_c, counters, pstep, task, &task_rot[task],
                                     from_r);
   if (done) {
+    // done[task] = epoch; then, in completion order, ready list slot k =
+    // this task (done + ntask: int64 count, then ntask slots of (epoch << 24
+    // | task)) so that the update starts with the tasks that finish first
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
       asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(done + task), "l"(epoch) : "memory");
+      int64_t *rl = done + gridDim.x;
+      const unsigned long long k = atomicAdd((unsigned long long *)rl, 1ull);
+      asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(rl + 1 + k),
+                   "l"((epoch << 24) | task) : "memory");
     }
   }
 }

@@ -709,10 +709,12 @@ int jh_profile_end(double *ms, int64_t *count) {
 // the cycle engine's own area (engine 2 only).
 static int64_t ws_base_bytes(int64_t n, int w) {
   const int64_t ntask = n / w;  // b/2 with b = n / (w/2)
-  // H | V' ring (4) | rotation-count ring (4) | per-task done flags (engine 1)
+  // H | V' ring (4) | rotation-count ring (4) | per-task done flags + ready
+  // list (engine 1)
   // | second H, Gram chain states, per-cycle slab flags (engine 1, fused Gram)
   const int64_t ncyc = ntask / 2 > 0 ? ntask / 2 : 1;
-  return ntask * (int64_t)w * w * 8 * 5 + ntask * 8 * 4 + ntask * 8 + ntask * (int64_t)w * w * 8 +
+  return ntask * (int64_t)w * w * 8 * 5 + ntask * 8 * 4 + (2 * ntask + 1) * 8 +
+         ntask * (int64_t)w * w * 8 +
          ncyc * 2 * 640 * 8 + ncyc * 8 + 1024;
 }
 
@@ -880,7 +882,7 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
   double *Vring = Hbuf + (int64_t)ntask * ww;
   int64_t *rring = (int64_t *)(Vring + 4 * (int64_t)ntask * ww);
   int64_t *done = rring + 4 * (int64_t)ntask;
-  double *Hbuf2 = (double *)(done + ntask);
+  double *Hbuf2 = (double *)(done + 2 * ntask + 1);
   double *gstate = Hbuf2 + (int64_t)ntask * ww;
   int64_t *sflag = (int64_t *)(gstate + (int64_t)(ntask / 2) * 2 * 640);
   auto hb = [&](int i) { return (i % 2) ? Hbuf2 : Hbuf; };
@@ -895,7 +897,7 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
   // disables (per-kernel timing needs the kernels apart)
   const bool pdl = g_overlap;
   static int64_t epoch = 0;
-  if (pdl && !separate) cudaMemsetAsync(done, 0xff, sizeof(int64_t) * ntask, st);
+  if (pdl && !separate) cudaMemsetAsync(done, 0xff, sizeof(int64_t) * (2 * ntask + 1), st);
   // opt-in (JHSVD_GU=1): the update launch of p-step s also forms the
   // Grams of p-step s+1 (one pass over G per p-step, Gram chains handed
   // from row slab to row slab); bitwise equal but slower on B200 (the
@@ -916,7 +918,10 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
       prof_mark(st, 0, true);
     }
     const bool use_pdl = pdl && !separate;
-    if (use_pdl) epoch++;
+    if (use_pdl) {
+      epoch++;
+      cudaMemsetAsync(done + ntask, 0, sizeof(int64_t), st);  // ready-list count
+    }
     // (with the programmatic launch, class 1 times the inner Jacobi and the
     // overlapped update together)
     prof_mark(st, 1, false);

@@ -433,9 +433,28 @@ __global__ void __launch_bounds__(160, 2) k_update_mix(MixArgs a) {
       gu_cta(a.gu, i % a.gu.ncyc, i / a.gu.ncyc, S.v);
       return;
     }
-    if (a.done) wait_flag_cta(a.done + i % a.ntask, a.epoch);
+    int task = i % a.ntask, slab = i / a.ntask;
+    if (a.done) {
+      // tasks in the order the inner kernel finishes them (its ready list):
+      // G item i is slab i % nslab of the (i / nslab)-th finished task
+      __shared__ int s_task;
+      const int64_t *rl = a.done + a.ntask;
+      const int k = i / a.nslab_g;
+      slab = i % a.nslab_g;
+      if (threadIdx.x == 0) {
+        int64_t v;
+        for (;;) {
+          asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(rl + 1 + k) : "memory");
+          if ((v >> 24) == a.epoch) break;
+          __nanosleep(64);
+        }
+        s_task = (int)(v & 0xffffff);
+      }
+      __syncthreads();
+      task = s_task;
+    }
     update_tma_cta<kVW>(a.G, a.ldg, a.m, nullptr, 0, 0, a.pairs, a.Vbuf, a.trot, a.nslab_g,
-                        i % a.ntask, i / a.ntask, &S.g.ring[0][0][0], S.g.full, S.g.empty);
+                        task, slab, &S.g.ring[0][0][0], S.g.full, S.g.empty);
     return;
   }
   int i = (int)v0, q = 0;
