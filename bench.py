@@ -351,7 +351,10 @@ def run_ours(args, rank: int, world: int):
         g_host = host_in.t()  # m x n, column-major, pinned
         torch.cuda.empty_cache()
         et = []
-        for _ in range(args.steps):
+        # one untimed warm-up call: steady state of a process that solves
+        # repeatedly (pinned output buffers come from torch's caching host
+        # allocator; a first-ever call also pays ~0.9 s per 2 GB of page pinning)
+        for k in range((1 if args.warmup > 0 else 0) + args.steps):
             _barrier(world)
             t0 = time.perf_counter()
             if world == 1:
@@ -360,10 +363,14 @@ def run_ours(args, rank: int, world: int):
                 from paper_1401_2720_b200.distsim import run_distributed
 
                 r, _ = run_distributed(g_host, J.Signature(n, n_plus), world, cfg)
-            et.append(_max_over_ranks(time.perf_counter() - t0, world))
+            dt = _max_over_ranks(time.perf_counter() - t0, world)
+            if k >= (1 if args.warmup > 0 else 0):
+                et.append(dt)
             del r
         return {"value": statistics.mean(et), "unit": "s", "h2d_bytes_per_step": 8 * m * n,
-                "d2h_bytes_per_step": 8 * (n + m * n + n * n)}
+                "d2h_bytes_per_step": 8 * (n + m * n + n * n),
+                "note": ("public API block_jacobi on a pinned host factor: H2D of G, solve, "
+                         "sigma/U/V back to host, after one untimed warm-up call")}
 
     if rank != 0:
         del U, V, res
