@@ -945,6 +945,11 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
       }
       continue;
     }
+    // V work: pair j = (2j, 2j+1) is applied to its even row slabs in the
+    // launch of p-step 2j+2 and to its odd ones in that of 2j+3, so the V
+    // items of a launch never wait for the inner kernel still running;
+    // whatever is due later than the last p-step is flushed after it, in
+    // p-step order (launches of one stream run in order)
     int nsrc = 0, sa[2], k0[2], kstep[2];
     bool second[2];
     const double *VpA[2], *VpB[2];
@@ -960,10 +965,24 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
       kstep[nsrc] = kst;
       nsrc++;
     };
-    // the V rows of one launch must be disjoint across its sources: a last
-    // p-step without a partner goes to its own launch after the pair's
+    auto flush = [&](int i0, bool sec, int kk0, int kst) {  // a V-only launch
+      nsrc = 0;
+      add(i0, sec, kk0, kst);
+      prof_mark(st, 3, false);
+      launch_update_mix(G, ldg, 0, pairs, ntask, vp(i), rt(i), V, ldv, nv, outer, plan, b, nsrc,
+                        sa, second, VpA, rotA, VpB, rotB, k0, kstep, st);
+      prof_mark(st, 3, true);
+      g_launches += 1;
+    };
+    static const bool late_v = [] {  // JHSVD_VSCHED=0: pair j in launches 2j+1 / 2j+2
+      const char *e = getenv("JHSVD_VSCHED");
+      return !(e && e[0] == '0');
+    }();
     bool tail_single = false;
-    if (i % 2 == 1) {
+    if (late_v) {
+      if (i % 2 == 0 && i >= 2) add(i - 2, true, 0, 2);
+      if (i % 2 == 1 && i >= 3) add(i - 3, true, 1, 2);
+    } else if (i % 2 == 1) {
       add(i - 1, true, 0, last ? 1 : 2);  // pair (i-1, i): even slabs now, odd ones next
     } else {
       if (i >= 2) add(i - 2, true, 1, 2);  // odd slabs of pair (i-2, i-1)
@@ -981,12 +1000,15 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
                       epoch, s, gu_now ? hb(i + 1) : nullptr, gstate, sflag);
     prof_mark(st, use_pdl ? 1 : 2, true);
     g_launches += 3;
-    if (tail_single) {
-      prof_mark(st, 3, false);
-      launch_vpair(V, ldv, nv, outer, plan, b, s, false, vp(i), rt(i), nullptr, nullptr, st);
-      prof_mark(st, 3, true);
-      g_launches += 1;
+    if (last && late_v) {
+      if (i % 2 == 1) {
+        flush(i - 1, true, 0, 1);            // the last pair, all slabs
+      } else {
+        if (i >= 2) flush(i - 2, true, 1, 2);  // odd slabs of the previous pair
+        flush(i, false, 0, 1);                 // the last p-step alone
+      }
     }
+    if (tail_single) flush(i, false, 0, 1);
   }
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : -(int)e;
