@@ -69,7 +69,15 @@ void launch_update_mix(double *G, int64_t ldg, int64_t m, const int32_t *pairs, 
                        const int64_t *const *rotB, const int *k0, const int *kstep,
                        cudaStream_t st, const int64_t *done = nullptr, int64_t epoch = 0,
                        int cur_step = -1, double *Hnext = nullptr, double *gstate = nullptr,
-                       int64_t *sflag = nullptr);
+                       int64_t *sflag = nullptr, const int32_t *pairs_next = nullptr,
+                       const int32_t *colpos = nullptr, int64_t *gcnt = nullptr,
+                       double *Hgram = nullptr);
+// pairs_next != null: Gram CTAs of p-step cur_step + 1 (pairs_next) at the end
+// of the grid write Hgram once the G slabs of their block-columns' tasks
+// (colpos: [b] task of p-step cur_step per block-column) are done (gcnt:
+// ntask epoch-tagged counters)
+void launch_colpos(const int32_t *outer, int nsteps, int T, int b, int32_t *colpos,
+                   cudaStream_t st);
 // Hnext != null: the G items also form the Gram matrices of p-step
 // cur_step + 1 into Hnext (gstate: cycles x 2 x 640 doubles of chain state,
 // sflag: cycles int64, both scratch)

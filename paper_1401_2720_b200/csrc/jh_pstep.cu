@@ -712,10 +712,13 @@ static int64_t ws_base_bytes(int64_t n, int w) {
   // H | V' ring (4) | rotation-count ring (4) | per-task done flags + ready
   // list (engine 1)
   // | second H, Gram chain states, per-cycle slab flags (engine 1, fused Gram)
+  // | per-task G slab counters, block-column -> task tables (engine 1, Grams
+  // in the update launch)
   const int64_t ncyc = ntask / 2 > 0 ? ntask / 2 : 1;
+  const int64_t b = 2 * ntask;
   return ntask * (int64_t)w * w * 8 * 5 + ntask * 8 * 4 + (2 * ntask + 1) * 8 +
          ntask * (int64_t)w * w * 8 +
-         ncyc * 2 * 640 * 8 + ncyc * 8 + 1024;
+         ncyc * 2 * 640 * 8 + ncyc * 8 + ntask * 8 + (b > 1 ? b - 1 : 1) * b * 4 + 1024;
 }
 
 // Bytes of device workspace jh_block_sweep (engines 0 and 1) needs.
@@ -885,6 +888,8 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
   double *Hbuf2 = (double *)(done + 2 * ntask + 1);
   double *gstate = Hbuf2 + (int64_t)ntask * ww;
   int64_t *sflag = (int64_t *)(gstate + (int64_t)(ntask / 2) * 2 * 640);
+  int64_t *gcnt = sflag + (ntask / 2);
+  int32_t *colpos = (int32_t *)(gcnt + ntask);
   auto hb = [&](int i) { return (i % 2) ? Hbuf2 : Hbuf; };
   auto vp = [&](int i) { return Vring + (int64_t)(i % 4) * ntask * ww; };
   auto rt = [&](int i) { return rring + (int64_t)(i % 4) * ntask; };
@@ -909,10 +914,27 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
   }();
   const bool gu = fuse_gram && !separate && w == 32;
   if (gu) cudaMemsetAsync(sflag, 0xff, sizeof(int64_t) * (ntask / 2), st);
+  // Grams of p-step s+1 as trailing CTAs of the update launch of p-step s
+  // (each starts when the G slabs of the two tasks that wrote its
+  // block-columns are done), so the Gram pass overlaps the update's tail
+  // JHSVD_GMIX=1 / 0 forces it on / off; by default on for G of at most 2^26
+  // entries (512 MB), where it measured 1.5-3% faster; slower for larger G
+  // (16384^2: 2.16 vs 2.07 ms per p-step, profiles/r01/cycle_engine.md)
+  static const int gmix_env = [] {
+    const char *e = getenv("JHSVD_GMIX");
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
+  }();
+  const bool gmix = (gmix_env == 1 || (gmix_env < 0 && m * n <= (int64_t(1) << 26))) && !gu && !separate &&
+                    w == 32 && nsteps > 1;
+  if (gmix) {
+    cudaMemsetAsync(gcnt, 0, sizeof(int64_t) * ntask, st);
+    launch_colpos(outer + (int64_t)first_step * ntask * 2, nsteps, ntask, b, colpos, st);
+    g_launches += 1;
+  }
   for (int i = 0; i < nsteps; i++) {
     const int s = first_step + i;
     const int32_t *pairs = outer + (int64_t)s * ntask * 2;
-    if (!gu || i == 0) {
+    if ((!gu && !gmix) || i == 0) {
       prof_mark(st, 0, false);
       launch_gram_tma(G, ldg, m, pairs, ntask, w, hb(i), st);
       prof_mark(st, 0, true);
@@ -997,7 +1019,9 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
     const bool gu_now = gu && !last;
     launch_update_mix(G, ldg, m, pairs, ntask, vp(i), rt(i), V, ldv, nv, outer, plan, b, nsrc,
                       sa, second, VpA, rotA, VpB, rotB, k0, kstep, st, use_pdl ? done : nullptr,
-                      epoch, s, gu_now ? hb(i + 1) : nullptr, gstate, sflag);
+                      epoch, s, gu_now ? hb(i + 1) : nullptr, gstate, sflag,
+                      gmix && !last ? pairs + ntask * 2 : nullptr, colpos + (int64_t)i * b, gcnt,
+                      hb(i + 1));
     prof_mark(st, use_pdl ? 1 : 2, true);
     g_launches += 3;
     if (last && late_v) {

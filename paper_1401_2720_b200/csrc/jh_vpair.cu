@@ -394,6 +394,97 @@ __global__ void __launch_bounds__(160, 2) k_vpair(VpArgs a) {
   vpair_cta(a, blockIdx.x, blockIdx.y, *reinterpret_cast<VpSmem *>(smraw));
 }
 
+// ---- Gram of one task of the next p-step inside the update launch -----------------
+//
+// The K1 body (jh_tiles.cu, k_gram_tma<32, 2>) as a device function for the
+// mixed launch: warp 0 streams the pair through a 3-stage TMA ring, warps 1
+// and 2 own 5 lower 8x8 tiles each (one in-order DMMA chain per tile over
+// the rows), warps 3 and 4 have nothing to do.  It runs after the G-update
+// CTAs of the two tasks that last wrote its block-columns (per-task slab
+// counters), i.e. in the tail of the update launch instead of after it.
+
+// Increments an epoch-tagged counter ((epoch << 16) | count; a value with an
+// older epoch counts as 0) and returns the new count.
+__device__ __forceinline__ int tagged_inc(int64_t *p, int64_t epoch) {
+  unsigned long long *c = (unsigned long long *)p;
+  unsigned long long old = atomicAdd(c, 0ull);
+  for (;;) {
+    const unsigned long long nw = ((int64_t)(old >> 16) == epoch)
+                                      ? old + 1
+                                      : (((unsigned long long)epoch << 16) | 1ull);
+    const unsigned long long seen = atomicCAS(c, old, nw);
+    if (seen == old) return (int)(nw & 0xffff);
+    old = seen;
+  }
+}
+
+__device__ __forceinline__ void gram_cta32(const double *G, int64_t ldg, int64_t m, int p, int q,
+                                           double *H, double *sm, uint64_t *full,
+                                           uint64_t *empty) {
+  constexpr int W = 32, NW = 4, BW = 16, MY = GramTiles<W, NW>::MY;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int64_t nchunk = cdiv(m, kRch);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp > NW) return;
+  if (warp == 0) {
+    fence_async_global();  // the block-columns were just written by generic stores
+    for (int64_t c = 0; c < nchunk; c++) {
+      const int s = (int)(c % kStages);
+      if (c >= kStages) mbar_wait(&empty[s], (uint32_t)(((c / kStages) - 1) & 1));
+      const int64_t r0 = c * kRch;
+      const uint32_t bytes = (uint32_t)min64(kRch, m - r0) * 8u;
+      if (lane == 0) mbar_expect_tx(&full[s], bytes * W);
+      __syncwarp();
+      const int64_t col = lane < BW ? (int64_t)p * BW + lane : (int64_t)q * BW + (lane - BW);
+      bulk_g2s(sm + ((size_t)s * W + lane) * kLd, G + col * ldg + r0, bytes, &full[s]);
+    }
+    return;
+  }
+  const int cw = warp - 1;
+  double acc[MY][2];
+#pragma unroll
+  for (int i = 0; i < MY; i++) acc[i][0] = acc[i][1] = 0.0;
+  for (int64_t c = 0; c < nchunk; c++) {
+    const int s = (int)(c % kStages);
+    mbar_wait(&full[s], (uint32_t)((c / kStages) & 1));
+    const double *buf = sm + (size_t)s * W * kLd + (size_t)g * kLd + t;
+    const int nr = (int)min64(kRch, m - c * kRch);
+    switch (cw) {
+      case 0: gram_chunk<W, NW, 0>(buf, nr, acc, t); break;
+      case 1: gram_chunk<W, NW, 1>(buf, nr, acc, t); break;
+      case 2: gram_chunk<W, NW, 2>(buf, nr, acc, t); break;
+      default: gram_chunk<W, NW, 3>(buf, nr, acc, t); break;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  switch (cw) {
+    case 0: gram_store<W, NW, 0>(H, acc, g, t); break;
+    case 1: gram_store<W, NW, 1>(H, acc, g, t); break;
+    case 2: gram_store<W, NW, 2>(H, acc, g, t); break;
+    default: gram_store<W, NW, 3>(H, acc, g, t); break;
+  }
+}
+
+__global__ void k_colpos(const int32_t *__restrict__ outer, int nsteps, int T, int b,
+                         int32_t *__restrict__ colpos) {
+  const int64_t n = (int64_t)nsteps * T;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = i / T;
+    const int t = (int)(i - s * T);
+    colpos[s * b + outer[2 * i]] = t;
+    colpos[s * b + outer[2 * i + 1]] = t;
+  }
+}
+
 // ---- one launch: the G update of p-step s (per-task CTAs of the per-p-step
 // kernel) and V-pair row slabs (vpair_cta), interleaved over the grid so
 // that HBM-bound G slabs and DMMA-bound V slabs share the SMs
@@ -412,6 +503,13 @@ struct MixArgs {
   int nsrc, nV;
   int use_gu;  // G items are GU items (update of p-step s + Grams of p-step s+1)
   GuArgs gu;
+  // Gram items of the next p-step at the end of the grid (nGr of them)
+  int nGr;
+  const int32_t *pairs_next;  // pair table row of p-step s+1
+  const int32_t *colpos;      // [b]: task of p-step s holding block-column c
+  int64_t *gcnt;              // [ntask]: (gepoch << 16) | G slabs done
+  int64_t gepoch;
+  double *Hn;
 };
 
 union MixSmem {
@@ -426,6 +524,29 @@ __global__ void __launch_bounds__(160, 2) k_update_mix(MixArgs a) {
   extern __shared__ __align__(128) unsigned char smraw[];
   MixSmem &S = *reinterpret_cast<MixSmem *>(smraw);
   const int N = a.nG + a.nV, bid = blockIdx.x;
+  if (bid >= N) {
+    // Gram of task u of the next p-step, once its two block-columns are
+    // final (the G updates of the tasks holding them now, colpos, are done;
+    // a queue in completion order was slower: most Grams need a late task)
+    const int u = bid - N;
+    const int p = a.pairs_next[2 * u], q = a.pairs_next[2 * u + 1];
+    if (threadIdx.x == 0) {
+      const int64_t want = (a.gepoch << 16) | a.nslab_g;
+      const int src[2] = {a.colpos[p], a.colpos[q]};
+      for (int k = 0; k < 2; k++)
+        for (;;) {
+          int64_t v;
+          asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(a.gcnt + src[k])
+                       : "memory");
+          if (v == want) break;
+          __nanosleep(64);
+        }
+    }
+    __syncthreads();
+    gram_cta32(a.G, a.ldg, a.m, p, q, a.Hn + (int64_t)u * kVW * kVW, &S.g.ring[0][0][0],
+               S.g.full, S.g.empty);
+    return;
+  }
   const int64_t v0 = (int64_t)bid * a.nV / N, v1 = (int64_t)(bid + 1) * a.nV / N;
   if (v1 == v0) {
     const int i = bid - (int)v0;
@@ -455,6 +576,14 @@ __global__ void __launch_bounds__(160, 2) k_update_mix(MixArgs a) {
     }
     update_tma_cta<kVW>(a.G, a.ldg, a.m, nullptr, 0, 0, a.pairs, a.Vbuf, a.trot, a.nslab_g,
                         task, slab, &S.g.ring[0][0][0], S.g.full, S.g.empty);
+    if (a.nGr) {
+      // count this slab of the task as final (for the next p-step's Grams)
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        tagged_inc(a.gcnt + task, a.gepoch);
+      }
+    }
     return;
   }
   int i = (int)v0, q = 0;
@@ -467,6 +596,11 @@ __global__ void __launch_bounds__(160, 2) k_update_mix(MixArgs a) {
 }
 
 }  // namespace
+
+void launch_colpos(const int32_t *outer, int nsteps, int T, int b, int32_t *colpos,
+                   cudaStream_t st) {
+  k_colpos<<<256, 256, 0, st>>>(outer, nsteps, T, b, colpos);
+}
 
 void launch_vpair(double *V, int64_t ldv, int64_t nv, const int32_t *outer, const int32_t *plan,
                   int b, int sa, bool second, const double *VpA, const int64_t *rotA,
@@ -504,7 +638,9 @@ void launch_update_mix(double *G, int64_t ldg, int64_t m, const int32_t *pairs, 
                        const int64_t *const *rotA, const double *const *VpB,
                        const int64_t *const *rotB, const int *k0, const int *kstep,
                        cudaStream_t st, const int64_t *done, int64_t epoch, int cur_step,
-                       double *Hnext, double *gstate, int64_t *sflag) {
+                       double *Hnext, double *gstate, int64_t *sflag,
+                       const int32_t *pairs_next, const int32_t *colpos, int64_t *gcnt,
+                       double *Hgram) {
   MixArgs a{};
   a.done = done;
   a.epoch = epoch;
@@ -569,7 +705,16 @@ void launch_update_mix(double *G, int64_t ldg, int64_t m, const int32_t *pairs, 
     a.nV += v.ncyc * a.nk[a.nsrc];
     a.nsrc++;
   }
-  if (a.nG + a.nV == 0) return;
+  if (pairs_next && m > 0) {
+    static int64_t gepoch = 0;
+    a.nGr = ntask;
+    a.pairs_next = pairs_next;
+    a.colpos = colpos;
+    a.gcnt = gcnt;
+    a.gepoch = ++gepoch;
+    a.Hn = Hgram;
+  }
+  if (a.nG + a.nV + a.nGr == 0) return;
   const size_t smem = sizeof(MixSmem);
   static bool attr = false;
   if (!attr) {
@@ -577,7 +722,7 @@ void launch_update_mix(double *G, int64_t ldg, int64_t m, const int32_t *pairs, 
     attr = true;
   }
   if (!done) {
-    k_update_mix<<<a.nG + a.nV, 160, smem, st>>>(a);
+    k_update_mix<<<a.nG + a.nV + a.nGr, 160, smem, st>>>(a);
     return;
   }
   // programmatic dependent launch: may start while the inner kernel runs
@@ -585,7 +730,7 @@ void launch_update_mix(double *G, int64_t ldg, int64_t m, const int32_t *pairs, 
   cudaLaunchAttribute pdl[1];
   pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   pdl[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.gridDim = dim3(a.nG + a.nV);
+  cfg.gridDim = dim3(a.nG + a.nV + a.nGr);
   cfg.blockDim = dim3(160);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
