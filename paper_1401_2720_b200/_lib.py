@@ -52,6 +52,7 @@ SIGNATURES = {
     "jh_probe_latency": (_c_i32, [_c_p, _c_p]),
     "jh_probe_fastmath": (_c_i32, [_c_p, _c_p, _c_i64, _c_p, _c_p]),
     "jh_inner_profile": (_c_i32, [_c_i32, _c_p]),
+    "jh_inner5_profile": (_c_i32, [_c_i32, _c_p]),
     "jh_bench_inner": (_c_i32, [_c_i32, _c_p, _c_p, _c_p, _c_p, _c_i32, _c_i32, _c_i64, _c_p,
                                 _c_i32, _c_d, _c_p, _c_p]),
     "jh_launch_count": (ctypes.c_ulonglong, []),

@@ -5,12 +5,13 @@
 // and 4 (jh_inner.cu) give bitwise the same results and stay for A/B runs
 // (JHSVD_INNER=3/4).
 #include "jh_inner5.cuh"
+#include "jh_inner6.cuh"
 #include "jh_kernels.h"
 
 namespace jh {
 
 template <int W>
-__global__ void __launch_bounds__(InnerCfg5<W>::NTH)
+__global__ void __launch_bounds__(InnerCfg5<W>::NTH, 4)
 k_factor_inner5(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
                 int64_t *__restrict__ task_rot, const int32_t *__restrict__ pairs,
                 int64_t n_plus, const int32_t *__restrict__ inner, int inner_limit,
@@ -41,13 +42,66 @@ k_factor_inner5(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
   }
 }
 
+// Variant 6 (jh_inner6.cuh): the same task with warp 0 alone on the serial
+// chain (w <= 32, opt-in: JHSVD_I6=1; slower than variant 5 on B200, the
+// R columns then cost one warp's FP64 issue instead of four warps').
+template <int W>
+__global__ void __launch_bounds__(InnerCfg5<W>::NTH, 4)
+k_factor_inner6(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
+                int64_t *__restrict__ task_rot, const int32_t *__restrict__ pairs,
+                int64_t n_plus, const int32_t *__restrict__ inner, int inner_limit,
+                double tol_c, unsigned long long *counters, int pstep, bool from_r,
+                int64_t *done, int64_t epoch) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int task = blockIdx.x;
+  inner6_task<W, InnerCfg5<W>::NTH>(smraw, Hbuf + (size_t)task * W * W, Vbuf + (size_t)task * W * W,
+                                    pairs[2 * task], pairs[2 * task + 1], n_plus, inner,
+                                    inner_limit, tol_c, counters, pstep, task, &task_rot[task],
+                                    from_r);
+  if (done) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(done + task), "l"(epoch) : "memory");
+      int64_t *rl = done + gridDim.x;
+      const unsigned long long k = atomicAdd((unsigned long long *)rl, 1ull);
+      asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(rl + 1 + k),
+                   "l"((epoch << 24) | task) : "memory");
+    }
+  }
+}
+
 bool inner5_ok(int w) { return w == 16 || w == 32 || w == 64; }
+
+static bool use_inner6(int w) {
+  static const bool on = [] {
+    const char *e = getenv("JHSVD_I6");
+    return e && e[0] == '1';
+  }();
+  return on && w <= 32;
+}
 
 template <int W>
 static void launch_inner5_t(const double *Hbuf, double *Vbuf, int64_t *trot, const int32_t *pairs,
                            int ntask, int64_t n_plus, const int32_t *inner, int inner_limit,
                            double tol_c, unsigned long long *counters, int pstep,
                            cudaStream_t st, bool from_r, int64_t *done, int64_t epoch) {
+  if constexpr (W <= 32) {
+    if (use_inner6(W)) {
+      const size_t smem6 = sizeof(InnerSmem6<W>);
+      static bool attr6 = false;
+      if (!attr6) {
+        cudaFuncSetAttribute(k_factor_inner6<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem6);
+        attr6 = true;
+      }
+      k_factor_inner6<W><<<ntask, InnerCfg5<W>::NTH, smem6, st>>>(
+          Hbuf, Vbuf, trot, pairs, n_plus, inner, inner_limit, tol_c, counters, pstep, from_r,
+          done, epoch);
+      return;
+    }
+  }
   const size_t smem = sizeof(InnerSmem5<W>);
   static bool attr = false;
   if (!attr) {
@@ -90,11 +144,25 @@ extern "C" int jh_bench_inner(int variant, const double *Hbuf, double *Vbuf, int
   else if (variant == 4 && jh::inner4_ok(w))
     jh::launch_inner4(Hbuf, Vbuf, trot, pairs, ntask, w, n_plus, inner, inner_limit, tol_c,
                       counters, 0, st);
-  else if (variant == 5 && jh::inner5_ok(w))
+  else if ((variant == 5 || variant == 6) && jh::inner5_ok(w))
     jh::launch_inner5(Hbuf, Vbuf, trot, pairs, ntask, w, n_plus, inner, inner_limit, tol_c,
                       counters, 0, st);
   else
     return -1000;
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : -(int)e;
+}
+
+// Enable (1) / disable (0) the phase timing of K2 (g_i5 in jh_inner5.cuh);
+// when out != NULL, copies the 10 counters to host memory and resets them.
+extern "C" int jh_inner5_profile(int on, unsigned long long *out) {
+  cudaDeviceSynchronize();
+  if (out) {
+    cudaMemcpyFromSymbol(out, jh::g_i5, sizeof(unsigned long long) * 10);
+    unsigned long long z[10] = {};
+    cudaMemcpyToSymbol(jh::g_i5, z, sizeof(z));
+  }
+  cudaMemcpyToSymbol(jh::g_i5_on, &on, sizeof(int));
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : -(int)e;
 }

@@ -10,6 +10,13 @@
 
 namespace jh {
 
+// optional phase timing (jh_inner5_profile; one copy per translation unit):
+// cycles seen by thread 0 in [load + Cholesky, dots, rotation + test,
+// barrier 1, R apply + barrier 2], inner p-steps, inner sweeps, tasks, task
+// cycles (sum), task cycles (max)
+static __device__ int g_i5_on = 0;
+static __device__ unsigned long long g_i5[10];
+
 template <int W>
 struct InnerCfg5 {
   static constexpr int HALF = W / 2;
@@ -51,6 +58,46 @@ __device__ __forceinline__ void rot_apply5(double *M, int ld, int p, int q, int 
   } else {
     *mp = np;
     *mq = nq;
+  }
+}
+
+// Rotations of one inner p-step applied to row i of M for the pairs g,
+// g + G, g + 2G, ... (< HALF): all loads first, then the arithmetic and the
+// stores (a loop of rot_apply5 calls serialises on the possible aliasing of
+// each store with the next pair's loads).  Same arithmetic as rot_apply5.
+template <int HALF, int G>
+__device__ __forceinline__ void rot_apply_rows(double *M, int ld, const int8_t *pst,
+                                               const StepParams5 *prm, int g, int i) {
+  constexpr int MP = (HALF + G - 1) / G;
+  double vp[MP], vq[MP];
+  StepParams5 P[MP];
+  int cp[MP], cq[MP];
+#pragma unroll
+  for (int u = 0; u < MP; u++) {
+    const int pi = g + u * G;
+    if (pi < HALF) {
+      P[u] = prm[pi];
+      cp[u] = pst[2 * pi];
+      cq[u] = pst[2 * pi + 1];
+      vp[u] = M[cp[u] * ld + i];
+      vq[u] = M[cq[u] * ld + i];
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < MP; u++) {
+    const int pi = g + u * G;
+    if (pi < HALF && P[u].act) {
+      const double cs = P[u].cs, tn = P[u].tn;
+      const double sn = (P[u].act & 4) ? tn : -tn;
+      double np = fma(sn, vq[u], vp[u]), nq = fma(tn, vp[u], vq[u]);
+      if (cs != 1.0) {
+        np = np * cs;
+        nq = nq * cs;
+      }
+      const bool sw = (P[u].act & 3) == 2;
+      M[cp[u] * ld + i] = sw ? nq : np;
+      M[cq[u] * ld + i] = sw ? np : nq;
+    }
   }
 }
 
@@ -218,8 +265,7 @@ __device__ __noinline__ long long inner5_task(unsigned char *smem, const double 
         break;
       }
       // R update of this inner p-step (all threads)
-      for (int pi = rg; pi < HALF; pi += RGS)
-        if (cur[pi].act) rot_apply5(S.R, LD, st[2 * pi], st[2 * pi + 1], ri, cur[pi]);
+      rot_apply_rows<HALF, RGS>(S.R, LD, st, cur, rg, ri);
       __syncthreads();
     }
     if (status) break;
@@ -253,8 +299,7 @@ __device__ __noinline__ long long inner5_task(unsigned char *smem, const double 
     const int last = (gstep - 1) % NSTEP;
     const int8_t *pst = S.steps + last * W;
     const StepParams5 *prev = S.prm[(gstep - 1) & 1];
-    for (int pi = rg; pi < HALF; pi += RGS)
-      if (prev[pi].act) rot_apply5(S.V, LD, pst[2 * pi], pst[2 * pi + 1], ri, prev[pi]);
+    rot_apply_rows<HALF, RGS>(S.V, LD, pst, prev, rg, ri);
   }
   __syncthreads();
   for (int e = tid; e < W * W; e += NTH) {

@@ -417,7 +417,7 @@ def run_distributed(g_matrix, signature: Optional[Signature], g: int,
     if isinstance(g_matrix, torch.Tensor):
         G0 = g_matrix.to(dev, torch.float64).t().contiguous()
     else:
-        G0 = torch.from_numpy(np.ascontiguousarray(np.asarray(g_matrix, np.float64).T)).to(dev)
+        G0 = torch.from_numpy(np.array(np.asarray(g_matrix, np.float64).T, order="C")).to(dev)
     if not bool(torch.isfinite(G0).all()):
         raise ValueError("the input factor contains NaN or infinity")
     if dev.type == "cuda":

@@ -196,3 +196,43 @@ def test_dmma_probe_runs():
     torch.cuda.synchronize()
     mism = int((Dm != Df).sum())
     print(f"DMMA vs in-order fma: {mism} of {Dm.numel()} entries differ")
+
+
+@pytest.mark.parametrize("env", [{"JHSVD_I6": "1"}, {"JHSVD_ENGINE": "0", "JHSVD_I6": "1"},
+                                 {"JHSVD_GMIX": "0"}, {"JHSVD_GMIX": "1"}])
+def test_kernel_variants_bitwise_in_subprocess(env, solves_golden):
+    """Opt-in kernel variants (read once per process from the environment)
+    give the reference golden bitwise: inner variant 6, Grams in the update
+    launch on / off."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    code = (
+        "import json, hashlib, numpy as np, sys\n"
+        "sys.path.insert(0, '.')\n"
+        "import paper_1401_2720_b200 as J\n"
+        "meta = json.load(open('tests/golden/solves.json'))\n"
+        "arrs = np.load('tests/golden/solves.npz')\n"
+        "sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()\n"
+        "out = {}\n"
+        "for name, m in meta.items():\n"
+        "    r = J.block_jacobi(arrs[name + '_in'], J.Signature(m['n'], m['n_plus']),\n"
+        "                       J.SolverConfig(**m['cfg']))\n"
+        "    out[name] = [sha(r.sigma), [list(s) for s in r.stats],\n"
+        "                 None if r.v is None else sha(np.asfortranarray(r.v).T)]\n"
+        "print(json.dumps(out))\n")
+    e = dict(os.environ)
+    e.update(env)
+    res = subprocess.run([sys.executable, "-c", code], cwd=root, env=e, capture_output=True,
+                         text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    got = json.loads(res.stdout.strip().splitlines()[-1])
+    gold, _ = solves_golden
+    for name, g in gold.items():
+        assert got[name][0] == g["sigma_sha256"], (name, env)
+        assert got[name][1] == g["stats"], (name, env)
+        assert got[name][2] == g["v_sha256"], (name, env)

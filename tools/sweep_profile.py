@@ -27,9 +27,16 @@ def main():
     solver = Solver(n, J.SolverConfig(), J.Signature(n, n_plus))
     eng = solver.engine
     lib = _lib.load_library()
+    lib.jh_set_overlap(0)  # kernels apart, so the classes separate
     G = G0.clone()
     V = torch.eye(n, dtype=torch.float64, device="cuda")
-    for sweep in range(30):
+    import os
+
+    phases = os.environ.get("INNER_PHASES") == "1"
+    nsw = int(os.environ.get("SWEEPS", "30"))
+    for sweep in range(nsw):
+        if phases:
+            lib.jh_inner5_profile(1, None)
         lib.jh_profile_begin(4 * eng.nsteps + 16)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -39,9 +46,23 @@ def main():
         ms = (ctypes.c_double * 4)()
         cnt = (ctypes.c_int64 * 4)()
         lib.jh_profile_end(ms, cnt)
+        if phases:
+            pv = (ctypes.c_uint64 * 10)()
+            lib.jh_inner5_profile(0, pv)
+            v = list(pv)
+            nst, nt = max(v[5], 1), max(v[7], 1)
+            print(json.dumps({"inner_phases": {
+                "tasks": v[7], "inner_sweeps_per_task": v[6] / nt,
+                "inner_steps_per_task": v[5] / nt,
+                "cycles_per_step": {k: round(v[i] / nst, 1) for i, k in
+                                    enumerate(["", "dots|wait_empty", "rotation|dots",
+                                               "barrier1|rotation", "apply_barrier2|v_wait_full"])
+                                    if i > 0},
+                "load_cholesky_cycles_per_task": v[0] / nt,
+                "task_cycles_avg": v[8] / nt, "task_cycles_max": v[9]}}), flush=True)
         print(json.dumps({"sweep": sweep + 1, "ms": e0.elapsed_time(e1), "rot": rot,
                           "proper": proper, "tasks_rotated": eng.tasks_rotated[-1],
-                          "gram_ms": ms[0], "inner_ms": ms[1], "update_ms": ms[2]}), flush=True)
+                          "gram_ms": ms[0], "inner_ms": ms[1], "update_ms": ms[2] + ms[3]}), flush=True)
         if proper == 0:
             break
 

@@ -17,14 +17,17 @@ def main():
     w = int(sys.argv[2]) if len(sys.argv) > 2 else 32
     sweeps = int(sys.argv[3]) if len(sys.argv) > 3 else 1
     steps = int(sys.argv[4]) if len(sys.argv) > 4 else None
+    import os
+
+    m = int(os.environ.get("M", n))  # rows (default square)
     cfg = SolverConfig(block_width=w)
     t0 = time.time()
-    outer = make_strategy("rrow", n // (w // 2))
+    outer = make_strategy(os.environ.get("OUTER", "rrow"), n // (w // 2))
     inner = make_strategy("rrow", w)
     print(f"strategy {time.time() - t0:.2f}s", flush=True)
-    eng = SweepEngine(n, n, n, cfg, outer, inner, n)
+    eng = SweepEngine(m, n, n, cfg, outer, inner, n)
     g = torch.Generator(device="cuda").manual_seed(0)
-    G = torch.randn(n, n, dtype=torch.float64, device="cuda", generator=g)
+    G = torch.randn(n, m, dtype=torch.float64, device="cuda", generator=g)
     V = torch.eye(n, dtype=torch.float64, device="cuda")
     # warm-up on a copy
     Gw, Vw = G.clone(), V.clone()
@@ -66,7 +69,7 @@ def main():
             per = pms[k] / max(pcnt[k], 1)
             extra = ""
             if k == 0:
-                gbs = ntask * 8.0 * w * n / (per / 1e3) / 1e9
+                gbs = ntask * 8.0 * w * m / (per / 1e3) / 1e9
                 extra = f" {gbs:.0f} GB/s"
             if k == 2:
                 gbs = nrot * 16.0 * w * 2 * n / (pms[k] / 1e3) / 1e9
