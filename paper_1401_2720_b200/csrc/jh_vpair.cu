@@ -165,18 +165,22 @@ __device__ __forceinline__ void vpair_cta(const VpArgs &a, int c, int k, VpSmem 
   }
   __syncthreads();
   if (warp == 0) {
+    // only the blocks some transform reads (late sweeps rotate few tasks)
+    const unsigned need = (updA[0] ? 0x3u : 0u) | (updA[1] ? 0xCu : 0u) | touchedB;
+    const uint32_t nneed = (uint32_t)__popc(need);
     for (int cc = 0; cc < nchunk; cc++) {
       const int st = cc % kVStages;
       if (cc >= kVStages) mbar_wait(&S.empty[st], (uint32_t)(((cc / kVStages) - 1) & 1));
       const int64_t r = r0 + (int64_t)cc * kRch;
       const uint32_t bytes = (uint32_t)min64(kRch, r1 - r) * 8u;
-      if (lane == 0) mbar_expect_tx(&S.full[st], bytes * kVCols);
+      if (lane == 0) mbar_expect_tx(&S.full[st], bytes * 16u * nneed);
       __syncwarp();
 #pragma unroll
       for (int h = 0; h < 2; h++) {
         const int j = lane + 32 * h;
-        bulk_g2s(&S.ring[st][j][0], a.V + (gcol[j >> 4] + (j & 15)) * a.ldv + r, bytes,
-                 &S.full[st]);
+        if ((need >> (j >> 4)) & 1u)
+          bulk_g2s(&S.ring[st][j][0], a.V + (gcol[j >> 4] + (j & 15)) * a.ldv + r, bytes,
+                   &S.full[st]);
       }
     }
     return;
