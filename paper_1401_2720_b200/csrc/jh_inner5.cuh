@@ -7,6 +7,7 @@
 #pragma once
 
 #include "jh_common.cuh"
+#include "jh_fastmath.cuh"
 
 namespace jh {
 
@@ -210,15 +211,26 @@ __device__ __noinline__ long long inner5_task(unsigned char *smem, const double 
           // orthogonality test (it has no side effects; a pair that passes
           // the test discards it, exactly like the reference never forms it)
           const bool hyp = S.sg[p] > 0 && S.sg[q] < 0;
-          double cs, tn;
-          const bool rot_ok = rotation_core(hpp, hqq, hpq, hyp ? -1.0 : 1.0, cs, tn);
+          // branch-free fast paths of the IEEE division / square root
+          // (jh_fastmath.cuh; the IEEE operators when an operand leaves
+          // their range): bitwise the same values, without the seven
+          // serialised slow-path regions
+          double cs, tn, sp, sq;
+          bool fast_ok;
+          bool rot_ok = rotation_core_fast(hpp, hqq, hpq, hyp ? -1.0 : 1.0, cs, tn, sp, sq,
+                                           fast_ok);
+          if (!fast_ok) {
+            rot_ok = rotation_core(hpp, hqq, hpq, hyp ? -1.0 : 1.0, cs, tn);
+            sp = sqrt(hpp);
+            sq = sqrt(hqq);
+          }
           if (hpp == 0.0) {
             fail = kZeroColumn;
             fb = p + 1;
           } else if (hqq == 0.0) {
             fail = kZeroColumn;
             fb = q + 1;
-          } else if (!(fabs(hpq) < tol_c * sqrt(hpp) * sqrt(hqq))) {
+          } else if (!(fabs(hpq) < tol_c * sp * sq)) {
             if (!rot_ok) {
               fail = kHypDomain;
               fb = p + 1;
