@@ -155,9 +155,10 @@ int jh_probe_rate(int kind, int ctas, int threads, int iters, double *out, void 
  * barrier, R apply, barrier; inner p-steps; inner sweeps; tasks).  on = 1
  * enables, 0 disables; out (host uint64[8]) receives and resets them. */
 int jh_inner_profile(int on, unsigned long long *out);
-// The same for the default inner kernel K2 (10 counters: cycles of thread 0
+// The same for the default inner kernel K2 (12 counters: cycles of thread 0
 // in load + Cholesky, dots, rotation + test, barrier 1, R apply + barrier 2;
-// inner p-steps, inner sweeps, tasks, task cycles sum, task cycles max).
+// inner p-steps, inner sweeps, tasks, task cycles sum, task cycles max, setup
+// cycles, Cholesky cycles; variant 6 only).
 int jh_inner5_profile(int on, unsigned long long *out);
 
 /* Diagnostic / test: branch-free division and sqrt fast paths vs the IEEE

@@ -154,12 +154,12 @@ extern "C" int jh_bench_inner(int variant, const double *Hbuf, double *Vbuf, int
 }
 
 // Enable (1) / disable (0) the phase timing of K2 (g_i5 in jh_inner5.cuh);
-// when out != NULL, copies the 10 counters to host memory and resets them.
+// when out != NULL, copies the 12 counters to host memory and resets them.
 extern "C" int jh_inner5_profile(int on, unsigned long long *out) {
   cudaDeviceSynchronize();
   if (out) {
-    cudaMemcpyFromSymbol(out, jh::g_i5, sizeof(unsigned long long) * 10);
-    unsigned long long z[10] = {};
+    cudaMemcpyFromSymbol(out, jh::g_i5, sizeof(unsigned long long) * 12);
+    unsigned long long z[12] = {};
     cudaMemcpyToSymbol(jh::g_i5, z, sizeof(z));
   }
   cudaMemcpyToSymbol(jh::g_i5_on, &on, sizeof(int));

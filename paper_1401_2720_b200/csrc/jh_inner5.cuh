@@ -11,12 +11,27 @@
 
 namespace jh {
 
+// IEEE a / b and sqrt(x) through the branch-free fast paths when they are in
+// range (bitwise the same values), the operators otherwise
+__device__ __forceinline__ double div_ieee(double a, double b) {
+  bool ok = true;
+  double q = div_fp(a, b, ok);
+  if (!ok) q = a / b;
+  return q;
+}
+__device__ __forceinline__ double sqrt_ieee(double x) {
+  bool ok = true;
+  double r = sqrt_fp(x, ok);
+  if (!ok) r = sqrt(x);
+  return r;
+}
+
 // optional phase timing (jh_inner5_profile; one copy per translation unit):
 // cycles seen by thread 0 in [load + Cholesky, dots, rotation + test,
 // barrier 1, R apply + barrier 2], inner p-steps, inner sweeps, tasks, task
 // cycles (sum), task cycles (max)
 static __device__ int g_i5_on = 0;
-static __device__ unsigned long long g_i5[10];
+static __device__ unsigned long long g_i5[12];
 
 template <int W>
 struct InnerCfg5 {
@@ -60,6 +75,62 @@ __device__ __forceinline__ void rot_apply5(double *M, int ld, int p, int q, int 
     *mp = np;
     *mq = nq;
   }
+}
+
+// Cholesky of the task's Gram matrix by one warp (reference element order:
+// element (j, x) receives its updates for pivots 0..j-1 in order, then the
+// square root or the division by l_j, as in the reference's forward-looking
+// loop; shuffles and warp syncs instead of CTA barriers);
+// writes R = L^T (zero strict lower triangle, ld W + 1) and returns 0, or
+// the 1-based index of the first bad pivot.  Lane x keeps column x of the
+// trailing triangle in registers, shifted by one row per pivot so that the
+// pivot row is always e[0]: the pivot loop stays rolled (the fully unrolled
+// form is ~10k instructions executed once per task, i.e. i-cache misses).
+// colk: W doubles of scratch shared memory.
+template <int W>
+__device__ __noinline__ int chol6_warp(const double *__restrict__ Hg, double *R, double *colk,
+                                      int lane) {
+  constexpr int LD = W + 1;
+  constexpr unsigned FULL = 0xffffffffu;
+  const int x = lane;
+  double e[W];  // e[j] = element (k + j, x) at pivot k
+#pragma unroll
+  for (int j = 0; j < W; j++) e[j] = (x < W && j <= x) ? __ldcg(Hg + j * W + x) : 0.0;
+  if (x < W)
+#pragma unroll
+    for (int i = 0; i < W; i++)
+      if (i > x) R[x * LD + i] = 0.0;
+  int chol = 0;
+#pragma unroll 1
+  for (int k = 0; k < W; k++) {
+    int bad = 0;
+    if (x == k) {
+      const double d = e[0];
+      if (!(d > 0.0) || !isfinite(d))
+        bad = 1;
+      else
+        e[0] = sqrt_ieee(d);
+    }
+    if (__shfl_sync(FULL, bad, k)) {
+      chol = k + 1;
+      break;
+    }
+    const double l = __shfl_sync(FULL, e[0], k);
+    if (x > k && x < W) e[0] = div_ieee(e[0], l);
+    if (x >= k && x < W) R[x * LD + k] = e[0];  // element (k, x) is final
+    colk[x] = e[0];                             // row k, element (k, x) per lane
+    __syncwarp();
+#pragma unroll
+    for (int j = 1; j < W; j++) {
+      const int jj = k + j;
+      if (jj < W && x >= jj) e[j] = fma(-e[0], colk[jj], e[j]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < W - 1; j++) e[j] = e[j + 1];
+    e[W - 1] = 0.0;
+  }
+  return chol;
 }
 
 // Rotations of one inner p-step applied to row i of M for the pairs g,
@@ -144,26 +215,36 @@ __device__ __noinline__ long long inner5_task(unsigned char *smem, const double 
     __syncthreads();
   } else {
 
-  // ---- forward-looking Cholesky (reference element order), lower triangle
-  {
-    const int x = tid % W, jg = tid / W;
-    constexpr int JS = NTH / W;
-    for (int k = 0; k < W; k++) {
-      if (tid == 0) {
-        const double d = S.H[k * W + k];
-        if (!(d > 0.0) || !isfinite(d))
-          S.chol = k + 1;
-        else
-          S.H[k * W + k] = sqrt(d);
+  if constexpr (W <= 32) {
+    // one warp, no CTA barriers (chol6_warp; H is read from global again,
+    // S.H serves as its scratch row)
+    if (warp == 0) {
+      const int c = chol6_warp<W>(Hg, S.R, S.H, lane);
+      if (lane == 0) S.chol = c;
+    }
+    __syncthreads();
+  } else {
+    // ---- forward-looking Cholesky (reference element order), lower triangle
+    {
+      const int x = tid % W, jg = tid / W;
+      constexpr int JS = NTH / W;
+      for (int k = 0; k < W; k++) {
+        if (tid == 0) {
+          const double d = S.H[k * W + k];
+          if (!(d > 0.0) || !isfinite(d))
+            S.chol = k + 1;
+          else
+            S.H[k * W + k] = sqrt_ieee(d);
+        }
+        __syncthreads();
+        if (S.chol) break;
+        const double l = S.H[k * W + k];
+        if (jg == 0 && x > k) S.H[k * W + x] = div_ieee(S.H[k * W + x], l);
+        __syncthreads();
+        for (int j = k + 1 + jg; j < W; j += JS)
+          if (x >= j) S.H[j * W + x] = fma(-S.H[k * W + x], S.H[k * W + j], S.H[j * W + x]);
+        __syncthreads();
       }
-      __syncthreads();
-      if (S.chol) break;
-      const double l = S.H[k * W + k];
-      if (jg == 0 && x > k) S.H[k * W + x] = S.H[k * W + x] / l;
-      __syncthreads();
-      for (int j = k + 1 + jg; j < W; j += JS)
-        if (x >= j) S.H[j * W + x] = fma(-S.H[k * W + x], S.H[k * W + j], S.H[j * W + x]);
-      __syncthreads();
     }
   }
   if (S.chol) {
@@ -173,12 +254,14 @@ __device__ __noinline__ long long inner5_task(unsigned char *smem, const double 
     }
     return -1;
   }
-  // R = L^T (R[i][j] = H[i * W + j] for i <= j)
-  for (int e = tid; e < W * W; e += NTH) {
-    const int j = e / W, i = e - j * W;
-    S.R[j * LD + i] = (i <= j) ? S.H[i * W + j] : 0.0;
+  if constexpr (W > 32) {
+    // R = L^T (R[i][j] = H[i * W + j] for i <= j)
+    for (int e = tid; e < W * W; e += NTH) {
+      const int j = e / W, i = e - j * W;
+      S.R[j * LD + i] = (i <= j) ? S.H[i * W + j] : 0.0;
+    }
+    __syncthreads();
   }
-  __syncthreads();
   }  // !from_r
 
   // ---- inner sweeps

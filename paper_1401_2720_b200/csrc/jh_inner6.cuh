@@ -45,49 +45,6 @@ __device__ __forceinline__ void named_bar_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-// Cholesky of the task's Gram matrix by one warp (see the header comment);
-// writes R = L^T (zero strict lower triangle, ld W + 1) and returns 0, or
-// the 1-based index of the first bad pivot.
-template <int W>
-__device__ __noinline__ int chol6_warp(const double *__restrict__ Hg, double *R, double *colk,
-                                      int lane) {
-  constexpr int LD = W + 1;
-  constexpr unsigned FULL = 0xffffffffu;
-  const int x = lane;
-  double e[W];  // e[j] = element (j, x), j <= x, of the triangle
-#pragma unroll
-  for (int j = 0; j < W; j++) e[j] = (x < W && j <= x) ? __ldcg(Hg + j * W + x) : 0.0;
-  int chol = 0;
-#pragma unroll
-  for (int k = 0; k < W; k++) {
-    // (no early exit: a break would keep the loop rolled and e[] in local
-    // memory; after a bad pivot the remaining columns are computed and dropped)
-    int bad = 0;
-    if (x == k) {
-      const double d = e[k];
-      if (!(d > 0.0) || !isfinite(d))
-        bad = 1;
-      else
-        e[k] = sqrt(d);
-    }
-    if (__shfl_sync(FULL, bad, k) && !chol) chol = k + 1;
-    const double l = __shfl_sync(FULL, e[k], k);
-    if (x > k && x < W) e[k] = e[k] / l;
-    colk[x] = e[k];  // row k of the factor, element (k, x) per lane
-    __syncwarp();
-#pragma unroll
-    for (int j = k + 1; j < W; j++) {
-      const double ekj = colk[j];  // element (k, j), a broadcast read
-      if (x >= j && x < W) e[j] = fma(-e[k], ekj, e[j]);
-    }
-    __syncwarp();
-  }
-  if (!chol && x < W)
-#pragma unroll
-    for (int i = 0; i < W; i++) R[x * LD + i] = (i <= x) ? e[i] : 0.0;
-  return chol;
-}
-
 // Returns the task's rotation count (>= 0; V' written to Vg column-major,
 // counters updated) or -1 after recording a numerical failure under key
 // (pstep, task_key).  smem must hold an InnerSmem6<W>.  All NTH threads call.
@@ -149,6 +106,7 @@ __device__ __forceinline__ long long inner6_task(unsigned char *smem, const doub
   }
 
   // ---- R: Cholesky of H (chain warp), or the given factor
+  long long t_setup = prof ? clock64() : 0;
   if (chain) {
     const int x = lane;
     if (from_r) {
@@ -159,6 +117,10 @@ __device__ __forceinline__ long long inner6_task(unsigned char *smem, const doub
     } else {
       const int chol = chol6_warp<W>(Hg, S.R[0], S.R[1], lane);
       if (lane == 0) S.chol = chol;
+      if (prof) {
+        atomicAdd(&g_i5[10], (unsigned long long)(t_setup - t_task));
+        atomicAdd(&g_i5[11], (unsigned long long)(clock64() - t_setup));
+      }
     }
   }
   __syncthreads();

@@ -47,7 +47,7 @@ def main():
         cnt = (ctypes.c_int64 * 4)()
         lib.jh_profile_end(ms, cnt)
         if phases:
-            pv = (ctypes.c_uint64 * 10)()
+            pv = (ctypes.c_uint64 * 12)()
             lib.jh_inner5_profile(0, pv)
             v = list(pv)
             nst, nt = max(v[5], 1), max(v[7], 1)
@@ -59,7 +59,9 @@ def main():
                                                "barrier1|rotation", "apply_barrier2|v_wait_full"])
                                     if i > 0},
                 "load_cholesky_cycles_per_task": v[0] / nt,
-                "task_cycles_avg": v[8] / nt, "task_cycles_max": v[9]}}), flush=True)
+                "task_cycles_avg": v[8] / nt, "task_cycles_max": v[9],
+                "setup_cycles_per_task": v[10] / nt, "cholesky_cycles_per_task": v[11] / nt}}),
+                  flush=True)
         print(json.dumps({"sweep": sweep + 1, "ms": e0.elapsed_time(e1), "rot": rot,
                           "proper": proper, "tasks_rotated": eng.tasks_rotated[-1],
                           "gram_ms": ms[0], "inner_ms": ms[1], "update_ms": ms[2] + ms[3]}), flush=True)
