@@ -8,10 +8,13 @@ or a CUDA device is missing.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 LIB_PATH = PKG / "_lib" / "libjhsvd_b200.so"
+if os.environ.get("JHSVD_LIB"):  # A/B runs against another build of the library
+    LIB_PATH = Path(os.environ["JHSVD_LIB"])
 
 
 class NativeUnavailable(RuntimeError):
