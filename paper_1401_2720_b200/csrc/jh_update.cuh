@@ -22,6 +22,7 @@ __device__ __forceinline__ void update_tma_cta(double *__restrict__ G, int64_t l
                                                const int32_t *__restrict__ pairs,
                                                const double *__restrict__ Vbuf,
                                                const int64_t *__restrict__ trot, int nslab_g,
+                                               int slab_rows,
                                                int task, int slab_y, double *ring,
                                                uint64_t *full, uint64_t *empty) {
   constexpr int NT = W / 8, NK = W / 4, BW = W / 2;
@@ -30,11 +31,11 @@ __device__ __forceinline__ void update_tma_cta(double *__restrict__ G, int64_t l
   double *A;
   int64_t ld, rows, s0;
   if (slab_y < nslab_g) {
-    A = G; ld = ldg; rows = m; s0 = (int64_t)slab_y * kUpdSlab;
+    A = G; ld = ldg; rows = m; s0 = (int64_t)slab_y * slab_rows;
   } else {
-    A = V; ld = ldv; rows = nv; s0 = (int64_t)(slab_y - nslab_g) * kUpdSlab;
+    A = V; ld = ldv; rows = nv; s0 = (int64_t)(slab_y - nslab_g) * slab_rows;
   }
-  const int64_t s1 = min64(s0 + kUpdSlab, rows);
+  const int64_t s1 = min64(s0 + slab_rows, rows);
   const int nchunk = (int)cdiv(s1 - s0, kRch);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   if (threadIdx.x == 0) {
@@ -113,7 +114,8 @@ k_update_tma(double *__restrict__ G, int64_t ldg, int64_t m, double *__restrict_
              const double *__restrict__ Vbuf, const int64_t *__restrict__ trot, int nslab_g) {
   extern __shared__ __align__(128) double ring[];  // [kUpdStages][W][kLd]
   __shared__ __align__(8) uint64_t full[kUpdStages], empty[kUpdStages];
-  update_tma_cta<W>(G, ldg, m, V, ldv, nv, pairs, Vbuf, trot, nslab_g, blockIdx.x, blockIdx.y,
+  update_tma_cta<W>(G, ldg, m, V, ldv, nv, pairs, Vbuf, trot, nslab_g, kUpdSlab, blockIdx.x,
+                    blockIdx.y,
                     ring, full, empty);
 }
 

@@ -49,7 +49,15 @@ __device__ __forceinline__ void wait_flag_cta(const int64_t *flag, int64_t epoch
 constexpr int kVW = 32;
 constexpr int kVCols = 64;
 constexpr int kVStages = 3;
-constexpr int kVSlab = 512;  // V rows per CTA (short CTAs: no long tail behind the G slabs)
+constexpr int kVSlab = 512;  // V rows per CTA of the separate V pass (launch_vpair)
+// Row slabs of the mixed launch: from 256 tasks per p-step on, longer G and
+// V slabs (fewer CTAs, less pipeline fill and drain per CTA); below that the
+// short ones keep enough CTAs for the SMs.  A/B at n = 16384 (ms per
+// p-step, G/V slab rows): 2048/512 1.952, 2048/1024 1.915, 4096/1024 1.89,
+// 4096/1536 1.882, 8192/2048 1.891; n = 4096: 4096/1536 is 8 % slower.
+constexpr int kMixBigTasks = 256;
+constexpr int kMixGSlab[2] = {2048, 4096};
+constexpr int kMixVSlab[2] = {512, 1536};
 
 struct VpSmem {
   double ring[kVStages][kVCols][kLd];
@@ -68,6 +76,7 @@ struct VpArgs {
   const int64_t *doneA;  // non-null: the step-a tasks may still be running
   const int64_t *doneB;  // non-null: the step-(a+1) tasks may still be running
   int64_t epoch;
+  int vslab;             // V rows per CTA
 };
 
 // rows 0..kRch-1 of the 32 slot columns col(k) = cb0 + k (k < 16),
@@ -153,7 +162,7 @@ __device__ __forceinline__ void vpair_cta(const VpArgs &a, int c, int k, VpSmem 
   unsigned touchedB = 0;
   for (int h = 0; h < 2; h++)
     if (updB[h]) touchedB |= (1u << ib[h][0]) | (1u << ib[h][1]);
-  const int64_t r0 = (int64_t)k * kVSlab, r1 = min64(r0 + kVSlab, a.nv);
+  const int64_t r0 = (int64_t)k * a.vslab, r1 = min64(r0 + a.vslab, a.nv);
   const int nchunk = (int)cdiv(r1 - r0, kRch);
   if (threadIdx.x == 0) {
     for (int i = 0; i < kVStages; i++) {
@@ -501,7 +510,7 @@ struct MixArgs {
   const int64_t *trot;
   const int64_t *done;  // non-null: launched programmatically after the inner kernel
   int64_t epoch;
-  int ntask, nslab_g, nG;
+  int ntask, nslab_g, nG, gslab;
   VpArgs vp[2];
   int k0[2], kstep[2], nk[2];
   int nsrc, nV;
@@ -578,7 +587,7 @@ __global__ void __launch_bounds__(160, 2) k_update_mix(MixArgs a) {
       __syncthreads();
       task = s_task;
     }
-    update_tma_cta<kVW>(a.G, a.ldg, a.m, nullptr, 0, 0, a.pairs, a.Vbuf, a.trot, a.nslab_g,
+    update_tma_cta<kVW>(a.G, a.ldg, a.m, nullptr, 0, 0, a.pairs, a.Vbuf, a.trot, a.nslab_g, a.gslab,
                         task, slab, &S.g.ring[0][0][0], S.g.full, S.g.empty);
     if (a.nGr) {
       // count this slab of the task as final (for the next p-step's Grams)
@@ -625,6 +634,7 @@ void launch_vpair(double *V, int64_t ldv, int64_t nv, const int32_t *outer, cons
   a.VpB = VpB ? VpB : VpA;
   a.rotA = rotA;
   a.rotB = rotB ? rotB : rotA;
+  a.vslab = kVSlab;
   const size_t smem = sizeof(VpSmem);
   static bool attr = false;
   if (!attr) {
@@ -655,7 +665,11 @@ void launch_update_mix(double *G, int64_t ldg, int64_t m, const int32_t *pairs, 
   a.Vbuf = Vbuf;
   a.trot = trot;
   a.ntask = ntask;
-  a.nslab_g = (int)cdiv(m, kUpdSlab);
+  const int big = ntask >= kMixBigTasks ? 1 : 0;  // a function of ntask only: the
+  // flush launches (m = 0) must cut V into the same slabs as the others
+  a.gslab = kMixGSlab[big];
+  const int vslab = kMixVSlab[big];
+  a.nslab_g = (int)cdiv(m, a.gslab);
   a.nG = ntask * a.nslab_g;
   if (Hnext) {
     // G update fused with the Grams of the next p-step
@@ -682,9 +696,10 @@ void launch_update_mix(double *G, int64_t ldg, int64_t m, const int32_t *pairs, 
     u.nslab = (int)cdiv(m, kGuSlab);
     a.nG = u.ncyc * u.nslab;
   }
-  const int nslab_v = (int)cdiv(nv, kVSlab);
+  const int nslab_v = (int)cdiv(nv, vslab);
   for (int q = 0; q < nsrc && V; q++) {
     VpArgs &v = a.vp[a.nsrc];
+    v.vslab = vslab;
     v.V = V;
     v.ldv = ldv;
     v.nv = nv;
