@@ -16,7 +16,7 @@ constexpr int kUpdSlab = 2048;     // rows per CTA
 // the body of one CTA (task, slab_y); ring = kUpdStages x W x kLd doubles of
 // shared memory, full / empty = kUpdStages mbarriers each (shared with the
 // mixed update kernel of jh_vpair.cu)
-template <int W>
+template <int W, int STAGES = kUpdStages>
 __device__ __forceinline__ void update_tma_cta(double *__restrict__ G, int64_t ldg, int64_t m,
                                                double *__restrict__ V, int64_t ldv, int64_t nv,
                                                const int32_t *__restrict__ pairs,
@@ -39,7 +39,7 @@ __device__ __forceinline__ void update_tma_cta(double *__restrict__ G, int64_t l
   const int nchunk = (int)cdiv(s1 - s0, kRch);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kUpdStages; s++) {
+    for (int s = 0; s < STAGES; s++) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kUpdCons);
     }
@@ -49,8 +49,8 @@ __device__ __forceinline__ void update_tma_cta(double *__restrict__ G, int64_t l
   if (warp == 0) {
     // producer
     for (int c = 0; c < nchunk; c++) {
-      const int s = c % kUpdStages;
-      if (c >= kUpdStages) mbar_wait(&empty[s], (uint32_t)(((c / kUpdStages) - 1) & 1));
+      const int s = c % STAGES;
+      if (c >= STAGES) mbar_wait(&empty[s], (uint32_t)(((c / STAGES) - 1) & 1));
       const int64_t r0 = s0 + (int64_t)c * kRch;
       const uint32_t bytes = (uint32_t)min64(kRch, s1 - r0) * 8u;
       if (lane == 0) mbar_expect_tx(&full[s], bytes * W);
@@ -73,8 +73,8 @@ __device__ __forceinline__ void update_tma_cta(double *__restrict__ G, int64_t l
   double *pout = A + ((int64_t)p * BW + 2 * t) * ld;
   double *qout = A + ((int64_t)q * BW + 2 * t) * ld;
   for (int c = 0; c < nchunk; c++) {
-    const int s = c % kUpdStages;
-    mbar_wait(&full[s], (uint32_t)((c / kUpdStages) & 1));
+    const int s = c % STAGES;
+    mbar_wait(&full[s], (uint32_t)((c / STAGES) & 1));
     const int64_t r0 = s0 + (int64_t)c * kRch;
     const double *buf = ring + (size_t)s * W * kLd;
 #pragma unroll

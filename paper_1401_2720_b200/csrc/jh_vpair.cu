@@ -56,6 +56,14 @@ constexpr int kVSlab = 512;  // V rows per CTA of the separate V pass (launch_vp
 // p-step, G/V slab rows): 2048/512 1.952, 2048/1024 1.915, 4096/1024 1.89,
 // 4096/1536 1.882, 8192/2048 1.891; n = 4096: 4096/1536 is 8 % slower.
 constexpr int kMixBigTasks = 256;
+#ifndef JH_MGST
+#define JH_MGST 6
+#endif
+constexpr int kMixGStages = JH_MGST;
+#ifndef JH_VORDER
+#define JH_VORDER 0
+#endif
+constexpr int kMixVOrder = JH_VORDER;  // ring stages of the G items (the union with the V ring)
 constexpr int kMixGSlab[2] = {2048, 4096};
 constexpr int kMixVSlab[2] = {512, 1536};
 
@@ -527,8 +535,8 @@ struct MixArgs {
 
 union MixSmem {
   struct {
-    double ring[kUpdStages][kVW][kLd];
-    uint64_t full[kUpdStages], empty[kUpdStages];
+    double ring[kMixGStages][kVW][kLd];
+    uint64_t full[kMixGStages], empty[kMixGStages];
   } g;
   VpSmem v;
 };
@@ -560,7 +568,16 @@ __global__ void __launch_bounds__(160, 2) k_update_mix(MixArgs a) {
                S.g.full, S.g.empty);
     return;
   }
-  const int64_t v0 = (int64_t)bid * a.nV / N, v1 = (int64_t)(bid + 1) * a.nV / N;
+  // item order: V items spread evenly among the G items, or (JH_VORDER 1)
+  // all V items first -- they do not wait for the inner kernel
+  int64_t v0, v1;
+  if (kMixVOrder == 1) {
+    v0 = bid < a.nV ? bid : a.nV;
+    v1 = bid < a.nV ? bid + 1 : a.nV;
+  } else {
+    v0 = (int64_t)bid * a.nV / N;
+    v1 = (int64_t)(bid + 1) * a.nV / N;
+  }
   if (v1 == v0) {
     const int i = bid - (int)v0;
     if (a.use_gu) {
@@ -587,7 +604,8 @@ __global__ void __launch_bounds__(160, 2) k_update_mix(MixArgs a) {
       __syncthreads();
       task = s_task;
     }
-    update_tma_cta<kVW>(a.G, a.ldg, a.m, nullptr, 0, 0, a.pairs, a.Vbuf, a.trot, a.nslab_g, a.gslab,
+    update_tma_cta<kVW, kMixGStages>(a.G, a.ldg, a.m, nullptr, 0, 0, a.pairs, a.Vbuf, a.trot,
+                                     a.nslab_g, a.gslab,
                         task, slab, &S.g.ring[0][0][0], S.g.full, S.g.empty);
     if (a.nGr) {
       // count this slab of the task as final (for the next p-step's Grams)
