@@ -10,8 +10,11 @@
 
 namespace jh {
 
+#ifndef JH_I5_MINB
+#define JH_I5_MINB 4
+#endif
 template <int W>
-__global__ void __launch_bounds__(InnerCfg5<W>::NTH, 4)
+__global__ void __launch_bounds__(InnerCfg5<W>::NTH, JH_I5_MINB)
 k_factor_inner5(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
                 int64_t *__restrict__ task_rot, const int32_t *__restrict__ pairs,
                 int64_t n_plus, const int32_t *__restrict__ inner, int inner_limit,

@@ -9,6 +9,10 @@
 #include "jh_common.cuh"
 #include "jh_fastmath.cuh"
 
+#ifndef JH_I5_ROLLED
+#define JH_I5_ROLLED 1
+#endif
+
 namespace jh {
 
 // IEEE a / b and sqrt(x) through the branch-free fast paths when they are in
@@ -359,8 +363,15 @@ __device__ __noinline__ long long inner5_task(unsigned char *smem, const double 
         bad = S.fail_bad;
         break;
       }
-      // R update of this inner p-step (all threads)
+      // R update of this inner p-step (all threads); the per-pair loop
+      // (JH_I5_ROLLED, default) keeps K2 at 104 registers and measured as
+      // fast as the batched form at n = 16384 (275 vs 285 us per launch)
+#if JH_I5_ROLLED
+      for (int pi = rg; pi < HALF; pi += RGS)
+        if (cur[pi].act) rot_apply5(S.R, LD, st[2 * pi], st[2 * pi + 1], ri, cur[pi]);
+#else
       rot_apply_rows<HALF, RGS>(S.R, LD, st, cur, rg, ri);
+#endif
       __syncthreads();
     }
     if (status) break;
