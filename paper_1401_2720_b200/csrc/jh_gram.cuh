@@ -13,6 +13,7 @@ constexpr int kRch = 64;          // rows per staged chunk
 constexpr int kLd = kRch + 4;     // padded smem column stride (doubles)
 constexpr int kStages = 3;
 
+
 // Consumer side of the Gram for warp WARP of NW: it owns tiles i = WARP
 // (mod NW) of the (W/8)(W/8+1)/2 lower tiles (enumerated row-major, X >= Y).
 template <int W, int NW>
@@ -22,10 +23,10 @@ struct GramTiles {
   static constexpr int MY = (NTILE + NW - 1) / NW;
 };
 
-template <int W, int NW, int WARP>
+template <int W, int NW, int WARP, int RCH = kRch>
 __device__ __forceinline__ void gram_chunk(const double *buf, int nr, double (&acc)[GramTiles<W, NW>::MY][2],
                                            int t) {
-  constexpr int NT = W / 8;
+  constexpr int NT = W / 8, LD = RCH + 4;
   auto tiles = [&](const double (&f)[NT]) {
     int i = 0, mine = 0;
 #pragma unroll
@@ -41,23 +42,23 @@ __device__ __forceinline__ void gram_chunk(const double *buf, int nr, double (&a
     double f[NT];
     const bool ok = !guard || (4 * kk + t < nr);
 #pragma unroll
-    for (int X = 0; X < NT; X++) f[X] = ok ? buf[X * 8 * kLd + 4 * kk] : 0.0;
+    for (int X = 0; X < NT; X++) f[X] = ok ? buf[X * 8 * LD + 4 * kk] : 0.0;
     tiles(f);
   };
-  if (nr == kRch) {
+  if (nr == RCH) {
     // explicit two-stage register pipeline: fragments of k-step kk+1 are
     // loaded before the DMMAs of k-step kk are issued
     double fa[NT], fb[NT];
 #pragma unroll
-    for (int X = 0; X < NT; X++) fa[X] = buf[X * 8 * kLd];
+    for (int X = 0; X < NT; X++) fa[X] = buf[X * 8 * LD];
 #pragma unroll
-    for (int kk = 0; kk < kRch / 4; kk += 2) {
+    for (int kk = 0; kk < RCH / 4; kk += 2) {
 #pragma unroll
-      for (int X = 0; X < NT; X++) fb[X] = buf[X * 8 * kLd + 4 * (kk + 1)];
+      for (int X = 0; X < NT; X++) fb[X] = buf[X * 8 * LD + 4 * (kk + 1)];
       tiles(fa);
-      if (kk + 2 < kRch / 4) {
+      if (kk + 2 < RCH / 4) {
 #pragma unroll
-        for (int X = 0; X < NT; X++) fa[X] = buf[X * 8 * kLd + 4 * (kk + 2)];
+        for (int X = 0; X < NT; X++) fa[X] = buf[X * 8 * LD + 4 * (kk + 2)];
       }
       tiles(fb);
     }

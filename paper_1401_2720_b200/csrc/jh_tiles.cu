@@ -30,20 +30,20 @@ namespace jh {
 // LDS.64 each) and issues one DMMA per tile: fragment X serves as the A
 // operand (A^T rows) and the B operand alike.
 
-template <int W, int NW>
+template <int W, int NW, int kGramRch, int kGramStages>
 __global__ void __launch_bounds__(32 * (NW + 1))
 k_gram_tma(const double *__restrict__ G, int64_t ldg, int64_t m,
            const int32_t *__restrict__ pairs, double *__restrict__ Hbuf) {
   // warp 0 produces (TMA bulk copies), warps 1..NW consume (DMMA)
-  constexpr int BW = W / 2, MY = GramTiles<W, NW>::MY;
-  extern __shared__ __align__(128) double sm[];  // [kStages][W][kLd]
-  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  constexpr int BW = W / 2, MY = GramTiles<W, NW>::MY, kGramLd = kGramRch + 4;
+  extern __shared__ __align__(128) double sm[];  // [kGramStages][W][kGramLd]
+  __shared__ __align__(8) uint64_t full[kGramStages], empty[kGramStages];
   const int task = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int p = pairs[2 * task], q = pairs[2 * task + 1];
-  const int64_t nchunk = cdiv(m, kRch);
+  const int64_t nchunk = cdiv(m, kGramRch);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; s++) {
+    for (int s = 0; s < kGramStages; s++) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NW);
     }
@@ -52,15 +52,15 @@ k_gram_tma(const double *__restrict__ G, int64_t ldg, int64_t m,
   __syncthreads();
   if (warp == 0) {
     for (int64_t c = 0; c < nchunk; c++) {
-      const int s = (int)(c % kStages);
-      if (c >= kStages) mbar_wait(&empty[s], (uint32_t)(((c / kStages) - 1) & 1));
-      const int64_t r0 = c * kRch;
-      const uint32_t bytes = (uint32_t)min64(kRch, m - r0) * 8u;
+      const int s = (int)(c % kGramStages);
+      if (c >= kGramStages) mbar_wait(&empty[s], (uint32_t)(((c / kGramStages) - 1) & 1));
+      const int64_t r0 = c * kGramRch;
+      const uint32_t bytes = (uint32_t)min64(kGramRch, m - r0) * 8u;
       if (lane == 0) mbar_expect_tx(&full[s], bytes * W);
       __syncwarp();
       for (int j = lane; j < W; j += 32) {
         const int64_t col = j < BW ? (int64_t)p * BW + j : (int64_t)q * BW + (j - BW);
-        bulk_g2s(sm + ((size_t)s * W + j) * kLd, G + col * ldg + r0, bytes, &full[s]);
+        bulk_g2s(sm + ((size_t)s * W + j) * kGramLd, G + col * ldg + r0, bytes, &full[s]);
       }
     }
     return;
@@ -71,18 +71,18 @@ k_gram_tma(const double *__restrict__ G, int64_t ldg, int64_t m,
   for (int i = 0; i < MY; i++) acc[i][0] = acc[i][1] = 0.0;
 
   for (int64_t c = 0; c < nchunk; c++) {
-    const int s = (int)(c % kStages);
-    mbar_wait(&full[s], (uint32_t)((c / kStages) & 1));
-    const double *buf = sm + (size_t)s * W * kLd + (size_t)g * kLd + t;
-    const int nr = (int)min64(kRch, m - c * kRch);
+    const int s = (int)(c % kGramStages);
+    mbar_wait(&full[s], (uint32_t)((c / kGramStages) & 1));
+    const double *buf = sm + (size_t)s * W * kGramLd + (size_t)g * kGramLd + t;
+    const int nr = (int)min64(kGramRch, m - c * kGramRch);
     if (cw == 0)
-      gram_chunk<W, NW, 0>(buf, nr, acc, t);
+      gram_chunk<W, NW, 0, kGramRch>(buf, nr, acc, t);
     else if (NW > 1 && cw == 1)
-      gram_chunk<W, NW, (NW > 1 ? 1 : 0)>(buf, nr, acc, t);
+      gram_chunk<W, NW, (NW > 1 ? 1 : 0), kGramRch>(buf, nr, acc, t);
     else if (NW > 2 && cw == 2)
-      gram_chunk<W, NW, (NW > 2 ? 2 : 0)>(buf, nr, acc, t);
+      gram_chunk<W, NW, (NW > 2 ? 2 : 0), kGramRch>(buf, nr, acc, t);
     else if (NW > 3 && cw == 3)
-      gram_chunk<W, NW, (NW > 3 ? 3 : 0)>(buf, nr, acc, t);
+      gram_chunk<W, NW, (NW > 3 ? 3 : 0), kGramRch>(buf, nr, acc, t);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
@@ -208,17 +208,34 @@ bool gram_tma_ok(int w, int64_t m, int64_t ldg) {
 // tasks meet long columns (tall factors: one CTA per task leaves SMs short
 // of DMMA warps while every tile is a chain over all m rows); JHSVD_GRAM_NW
 // overrides
-template <int W, int NW>
+template <int W, int NW, int RCH, int STG>
 static void launch_gram_nw(const double *G, int64_t ldg, int64_t m, const int32_t *pairs,
                            int ntask, double *Hbuf, cudaStream_t st) {
-  const size_t smem = sizeof(double) * (size_t)kStages * W * kLd;
+  const size_t smem = sizeof(double) * (size_t)STG * W * (RCH + 4);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_gram_tma<W, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_gram_tma<W, NW, RCH, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     attr = true;
   }
-  k_gram_tma<W, NW><<<ntask, 32 * (NW + 1), smem, st>>>(G, ldg, m, pairs, Hbuf);
+  k_gram_tma<W, NW, RCH, STG><<<ntask, 32 * (NW + 1), smem, st>>>(G, ldg, m, pairs, Hbuf);
+}
+
+// Ring shape by the CTAs an SM must hold for one wave: longer chunks (one
+// bulk copy of 8 * rows bytes per column) pay while the ring still fits
+// (w = 32: 192 rows x 2 stages = 100 KB up to 2 CTAs per SM, 128 x 2 up
+// to 3, 104 x 2 = 55 KB up to 4).  K1 us per launch, 64 x 3 before:
+// n = 16384 390.5 -> 376.4, 131072 x 8192 2079 -> 1766, n = 4096 72 -> 61.
+template <int W, int NW>
+static void launch_gram_shape(const double *G, int64_t ldg, int64_t m, const int32_t *pairs,
+                              int ntask, int sms, double *Hbuf, cudaStream_t st) {
+  const int per_sm = (ntask + sms - 1) / sms;
+  if (per_sm <= 2)
+    launch_gram_nw<W, NW, 192, 2>(G, ldg, m, pairs, ntask, Hbuf, st);
+  else if (per_sm == 3)
+    launch_gram_nw<W, NW, 128, 2>(G, ldg, m, pairs, ntask, Hbuf, st);
+  else
+    launch_gram_nw<W, NW, 104, 2>(G, ldg, m, pairs, ntask, Hbuf, st);
 }
 
 template <int W>
@@ -228,17 +245,18 @@ static void launch_gram_t(const double *G, int64_t ldg, int64_t m, const int32_t
     const char *e = getenv("JHSVD_GRAM_NW");
     return e ? atoi(e) : 0;
   }();
-  int nw = env_nw;
-  if (nw != 2 && nw != 4) {
-    int dev = 0, sms = 148;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    nw = (ntask < 3 * sms) ? 4 : 2;
   }
+  int nw = env_nw;
+  if (nw != 2 && nw != 4) nw = (ntask < 3 * sms) ? 4 : 2;
   if (nw == 4)
-    launch_gram_nw<W, 4>(G, ldg, m, pairs, ntask, Hbuf, st);
+    launch_gram_shape<W, 4>(G, ldg, m, pairs, ntask, sms, Hbuf, st);
   else
-    launch_gram_nw<W, 2>(G, ldg, m, pairs, ntask, Hbuf, st);
+    launch_gram_shape<W, 2>(G, ldg, m, pairs, ntask, sms, Hbuf, st);
 }
 
 void launch_gram_tma(const double *G, int64_t ldg, int64_t m, const int32_t *pairs, int ntask,
