@@ -16,7 +16,7 @@ constexpr int kUpdSlab = 2048;     // rows per CTA
 // the body of one CTA (task, slab_y); ring = kUpdStages x W x kLd doubles of
 // shared memory, full / empty = kUpdStages mbarriers each (shared with the
 // mixed update kernel of jh_vpair.cu)
-template <int W, int STAGES = kUpdStages>
+template <int W, int STAGES = kUpdStages, int RCH = kRch>
 __device__ __forceinline__ void update_tma_cta(double *__restrict__ G, int64_t ldg, int64_t m,
                                                double *__restrict__ V, int64_t ldv, int64_t nv,
                                                const int32_t *__restrict__ pairs,
@@ -25,7 +25,9 @@ __device__ __forceinline__ void update_tma_cta(double *__restrict__ G, int64_t l
                                                int slab_rows,
                                                int task, int slab_y, double *ring,
                                                uint64_t *full, uint64_t *empty) {
-  constexpr int NT = W / 8, NK = W / 4, BW = W / 2;
+  constexpr int NT = W / 8, NK = W / 4, BW = W / 2, LD = RCH + 4;
+  constexpr int RB = RCH / (8 * kUpdCons);  // 8-row blocks per consumer warp and chunk
+  static_assert(RCH % (8 * kUpdCons) == 0, "chunk rows");
   if (trot[task] == 0) return;
   const int p = pairs[2 * task], q = pairs[2 * task + 1];
   double *A;
@@ -36,7 +38,7 @@ __device__ __forceinline__ void update_tma_cta(double *__restrict__ G, int64_t l
     A = V; ld = ldv; rows = nv; s0 = (int64_t)(slab_y - nslab_g) * slab_rows;
   }
   const int64_t s1 = min64(s0 + slab_rows, rows);
-  const int nchunk = (int)cdiv(s1 - s0, kRch);
+  const int nchunk = (int)cdiv(s1 - s0, RCH);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; s++) {
@@ -51,13 +53,13 @@ __device__ __forceinline__ void update_tma_cta(double *__restrict__ G, int64_t l
     for (int c = 0; c < nchunk; c++) {
       const int s = c % STAGES;
       if (c >= STAGES) mbar_wait(&empty[s], (uint32_t)(((c / STAGES) - 1) & 1));
-      const int64_t r0 = s0 + (int64_t)c * kRch;
-      const uint32_t bytes = (uint32_t)min64(kRch, s1 - r0) * 8u;
+      const int64_t r0 = s0 + (int64_t)c * RCH;
+      const uint32_t bytes = (uint32_t)min64(RCH, s1 - r0) * 8u;
       if (lane == 0) mbar_expect_tx(&full[s], bytes * W);
       __syncwarp();
       for (int j = lane; j < W; j += 32) {
         const int64_t col = j < BW ? (int64_t)p * BW + j : (int64_t)q * BW + (j - BW);
-        bulk_g2s(ring + ((size_t)s * W + j) * kLd, A + col * ld + r0, bytes, &full[s]);
+        bulk_g2s(ring + ((size_t)s * W + j) * LD, A + col * ld + r0, bytes, &full[s]);
       }
     }
     return;
@@ -75,14 +77,14 @@ __device__ __forceinline__ void update_tma_cta(double *__restrict__ G, int64_t l
   for (int c = 0; c < nchunk; c++) {
     const int s = c % STAGES;
     mbar_wait(&full[s], (uint32_t)((c / STAGES) & 1));
-    const int64_t r0 = s0 + (int64_t)c * kRch;
-    const double *buf = ring + (size_t)s * W * kLd;
+    const int64_t r0 = s0 + (int64_t)c * RCH;
+    const double *buf = ring + (size_t)s * W * LD;
 #pragma unroll
-    for (int rb = 0; rb < 2; rb++) {
-      const int rl = cw * 16 + rb * 8;
+    for (int rb = 0; rb < RB; rb++) {
+      const int rl = cw * (8 * RB) + rb * 8;
       double a[NK];
 #pragma unroll
-      for (int kk = 0; kk < NK; kk++) a[kk] = buf[(4 * kk + t) * kLd + rl + g];
+      for (int kk = 0; kk < NK; kk++) a[kk] = buf[(4 * kk + t) * LD + rl + g];
       double acc[NT][2];
 #pragma unroll
       for (int Y = 0; Y < NT; Y++) acc[Y][0] = acc[Y][1] = 0.0;

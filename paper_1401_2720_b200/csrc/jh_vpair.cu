@@ -57,9 +57,13 @@ constexpr int kVSlab = 512;  // V rows per CTA of the separate V pass (launch_vp
 // 4096/1536 1.882, 8192/2048 1.891; n = 4096: 4096/1536 is 8 % slower.
 constexpr int kMixBigTasks = 256;
 #ifndef JH_MGST
-#define JH_MGST 6
+#define JH_MGST 3
 #endif
-constexpr int kMixGStages = JH_MGST;
+constexpr int kMixGStages = JH_MGST;  // ring stages of the G items (inside the union with the V ring)
+#ifndef JH_MGRCH
+#define JH_MGRCH 128
+#endif
+constexpr int kMixGRch = JH_MGRCH;  // rows per G-item chunk
 #ifndef JH_VORDER
 #define JH_VORDER 0
 #endif
@@ -535,7 +539,7 @@ struct MixArgs {
 
 union MixSmem {
   struct {
-    double ring[kMixGStages][kVW][kLd];
+    double ring[kMixGStages][kVW][kMixGRch + 4];
     uint64_t full[kMixGStages], empty[kMixGStages];
   } g;
   VpSmem v;
@@ -604,7 +608,8 @@ __global__ void __launch_bounds__(160, 2) k_update_mix(MixArgs a) {
       __syncthreads();
       task = s_task;
     }
-    update_tma_cta<kVW, kMixGStages>(a.G, a.ldg, a.m, nullptr, 0, 0, a.pairs, a.Vbuf, a.trot,
+    update_tma_cta<kVW, kMixGStages, kMixGRch>(a.G, a.ldg, a.m, nullptr, 0, 0, a.pairs, a.Vbuf,
+                                               a.trot,
                                      a.nslab_g, a.gslab,
                         task, slab, &S.g.ring[0][0][0], S.g.full, S.g.empty);
     if (a.nGr) {
