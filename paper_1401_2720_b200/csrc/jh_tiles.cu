@@ -273,7 +273,7 @@ template <int W>
 static void launch_update_tma_t(double *G, int64_t ldg, int64_t m, double *V, int64_t ldv,
                                 int64_t nv, const int32_t *pairs, int ntask, const double *Vbuf,
                                 const int64_t *trot, cudaStream_t st) {
-  const size_t smem = sizeof(double) * (size_t)kUpdStages * W * kLd;
+  const size_t smem = sizeof(double) * (size_t)kE0Stages * W * (kE0Rch + 4);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_update_tma<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -109,16 +109,24 @@ __device__ __forceinline__ void update_tma_cta(double *__restrict__ G, int64_t l
   }
 }
 
+// ring of the stand-alone update K3 (engine 0): chunk rows x stages
+#ifndef JH_E0RCH
+#define JH_E0RCH 128
+#endif
+#ifndef JH_E0STG
+#define JH_E0STG 3
+#endif
+constexpr int kE0Rch = JH_E0RCH, kE0Stages = JH_E0STG;
+
 template <int W>
 __global__ void __launch_bounds__(32 * (kUpdCons + 1))
 k_update_tma(double *__restrict__ G, int64_t ldg, int64_t m, double *__restrict__ V,
              int64_t ldv, int64_t nv, const int32_t *__restrict__ pairs,
              const double *__restrict__ Vbuf, const int64_t *__restrict__ trot, int nslab_g) {
-  extern __shared__ __align__(128) double ring[];  // [kUpdStages][W][kLd]
-  __shared__ __align__(8) uint64_t full[kUpdStages], empty[kUpdStages];
-  update_tma_cta<W>(G, ldg, m, V, ldv, nv, pairs, Vbuf, trot, nslab_g, kUpdSlab, blockIdx.x,
-                    blockIdx.y,
-                    ring, full, empty);
+  extern __shared__ __align__(128) double ring[];  // [kE0Stages][W][kE0Rch + 4]
+  __shared__ __align__(8) uint64_t full[kE0Stages], empty[kE0Stages];
+  update_tma_cta<W, kE0Stages, kE0Rch>(G, ldg, m, V, ldv, nv, pairs, Vbuf, trot, nslab_g,
+                                       kUpdSlab, blockIdx.x, blockIdx.y, ring, full, empty);
 }
 
 }  // namespace jh
