@@ -48,7 +48,15 @@ __device__ __forceinline__ void wait_flag_cta(const int64_t *flag, int64_t epoch
 
 constexpr int kVW = 32;
 constexpr int kVCols = 64;
-constexpr int kVStages = 3;
+#ifndef JH_VRCH
+#define JH_VRCH 64
+#endif
+#ifndef JH_VSTG
+#define JH_VSTG 3
+#endif
+constexpr int kVStages = JH_VSTG;    // ring stages of the V items
+constexpr int kVRch = JH_VRCH;       // rows per V-item chunk
+constexpr int kVLd = kVRch + 4;      // = 4 (mod 16): conflict-free 64-bit shared accesses
 constexpr int kVSlab = 512;  // V rows per CTA of the separate V pass (launch_vpair)
 // Row slabs of the mixed launch: from 256 tasks per p-step on, longer G and
 // V slabs (fewer CTAs, less pipeline fill and drain per CTA); below that the
@@ -72,7 +80,7 @@ constexpr int kMixGSlab[2] = {2048, 4096};
 constexpr int kMixVSlab[2] = {512, 1536};
 
 struct VpSmem {
-  double ring[kVStages][kVCols][kLd];
+  double ring[kVStages][kVCols][kVLd];
   uint64_t full[kVStages], adone[kVStages], empty[kVStages];
 };
 
@@ -91,7 +99,7 @@ struct VpArgs {
   int vslab;             // V rows per CTA
 };
 
-// rows 0..kRch-1 of the 32 slot columns col(k) = cb0 + k (k < 16),
+// rows 0..kVRch-1 of the 32 slot columns col(k) = cb0 + k (k < 16),
 // cb1 + k - 16 (k >= 16) times V' (fragments in registers); each result
 // entry goes to the slot in place when keep[block] and to HBM when
 // fin[block] (block = slot block of its column, 0..3)
@@ -102,14 +110,14 @@ __device__ __forceinline__ void vp_transform(double *buf, int cb0, int cb1,
                                              int t) {
   const int sw = (t >> 1) & 1;  // conflict-free 64-bit shared stores
 #pragma unroll 1
-  for (int rb = 0; rb < kRch / 8; rb += 2) {
+  for (int rb = 0; rb < kVRch / 8; rb += 2) {
     double a[2][8];
 #pragma unroll
     for (int h = 0; h < 2; h++)
 #pragma unroll
       for (int kk = 0; kk < 8; kk++) {
         const int col = (kk < 4 ? cb0 + 4 * kk : cb1 + 4 * kk - 16) + t;
-        a[h][kk] = buf[col * kLd + 8 * (rb + h) + g];
+        a[h][kk] = buf[col * kVLd + 8 * (rb + h) + g];
       }
     double acc[2][4][2];
 #pragma unroll
@@ -134,7 +142,7 @@ __device__ __forceinline__ void vp_transform(double *buf, int cb0, int cb1,
           const int j = jj ^ sw;
           const double v = j ? acc[h][Y][1] : acc[h][Y][0];
           const int n = 8 * (Y & 1) + 2 * t + j;
-          if (kp) buf[(cbase + n) * kLd + row] = v;
+          if (kp) buf[(cbase + n) * kVLd + row] = v;
           if (to_g) st_f64(V + (gcol[blk] + n) * ldv + r + row, v);
         }
       }
@@ -175,7 +183,7 @@ __device__ __forceinline__ void vpair_cta(const VpArgs &a, int c, int k, VpSmem 
   for (int h = 0; h < 2; h++)
     if (updB[h]) touchedB |= (1u << ib[h][0]) | (1u << ib[h][1]);
   const int64_t r0 = (int64_t)k * a.vslab, r1 = min64(r0 + a.vslab, a.nv);
-  const int nchunk = (int)cdiv(r1 - r0, kRch);
+  const int nchunk = (int)cdiv(r1 - r0, kVRch);
   if (threadIdx.x == 0) {
     for (int i = 0; i < kVStages; i++) {
       mbar_init(&S.full[i], 1);
@@ -192,8 +200,8 @@ __device__ __forceinline__ void vpair_cta(const VpArgs &a, int c, int k, VpSmem 
     for (int cc = 0; cc < nchunk; cc++) {
       const int st = cc % kVStages;
       if (cc >= kVStages) mbar_wait(&S.empty[st], (uint32_t)(((cc / kVStages) - 1) & 1));
-      const int64_t r = r0 + (int64_t)cc * kRch;
-      const uint32_t bytes = (uint32_t)min64(kRch, r1 - r) * 8u;
+      const int64_t r = r0 + (int64_t)cc * kVRch;
+      const uint32_t bytes = (uint32_t)min64(kVRch, r1 - r) * 8u;
       if (lane == 0) mbar_expect_tx(&S.full[st], bytes * 16u * nneed);
       __syncwarp();
 #pragma unroll
@@ -222,8 +230,8 @@ __device__ __forceinline__ void vpair_cta(const VpArgs &a, int c, int k, VpSmem 
     const uint32_t par = (uint32_t)((cc / kVStages) & 1);
     mbar_wait(phaseA ? &S.full[st] : &S.adone[st], par);
     double *buf = &S.ring[st][0][0];
-    const int64_t r = r0 + (int64_t)cc * kRch;
-    const int nr = (int)min64(kRch, r1 - r);
+    const int64_t r = r0 + (int64_t)cc * kVRch;
+    const int nr = (int)min64(kVRch, r1 - r);
     if (mine) vp_transform(buf, cb0, cb1, bf, keep, fin, a.V, a.ldv, gcol, r, nr, g, t);
     if (phaseA && mine && keep) fence_async_smem_cta();  // before the slot's next TMA fill
     __syncwarp();
@@ -268,7 +276,7 @@ __device__ __forceinline__ void gu_gram_tiles(const double *buf, int nr, const i
                                               double (&acc)[10][2], int g, int t) {
   const double *c[4];
 #pragma unroll
-  for (int X = 0; X < 4; X++) c[X] = buf + (cb[X] + g) * kLd + t;
+  for (int X = 0; X < 4; X++) c[X] = buf + (cb[X] + g) * kVLd + t;
   auto step = [&](int kk, bool ok) {
     double f[4];
 #pragma unroll
@@ -279,9 +287,9 @@ __device__ __forceinline__ void gu_gram_tiles(const double *buf, int nr, const i
 #pragma unroll
       for (int Y = 0; Y <= X; Y++, i++) dmma(acc[i][0], acc[i][1], f[X], f[Y]);
   };
-  if (nr == kRch) {
+  if (nr == kVRch) {
 #pragma unroll 2
-    for (int kk = 0; kk < kRch / 4; kk++) step(kk, true);
+    for (int kk = 0; kk < kVRch / 4; kk++) step(kk, true);
   } else {
     const int nks = (nr + 3) / 4;
     for (int kk = 0; kk < nks; kk++) step(kk, 4 * kk + t < nr);
@@ -303,7 +311,7 @@ __device__ __forceinline__ void gu_cta(const GuArgs &a, int c, int k, VpSmem &S)
   const bool updA[2] = {a.rotA[tk[0]] > 0, a.rotA[tk[1]] > 0};
   const int ib[2][2] = {{cy[4], cy[5]}, {cy[6], cy[7]}};
   const int64_t r0 = (int64_t)k * kGuSlab, r1 = min64(r0 + kGuSlab, a.m);
-  const int nchunk = (int)cdiv(r1 - r0, kRch);
+  const int nchunk = (int)cdiv(r1 - r0, kVRch);
   if (threadIdx.x == 0) {
     for (int i = 0; i < kVStages; i++) {
       mbar_init(&S.full[i], 1);
@@ -318,8 +326,8 @@ __device__ __forceinline__ void gu_cta(const GuArgs &a, int c, int k, VpSmem &S)
     for (int cc = 0; cc < nchunk; cc++) {
       const int st = cc % kVStages;
       if (cc >= kVStages) mbar_wait(&S.empty[st], (uint32_t)(((cc / kVStages) - 1) & 1));
-      const int64_t r = r0 + (int64_t)cc * kRch;
-      const uint32_t bytes = (uint32_t)min64(kRch, r1 - r) * 8u;
+      const int64_t r = r0 + (int64_t)cc * kVRch;
+      const uint32_t bytes = (uint32_t)min64(kVRch, r1 - r) * 8u;
       if (lane == 0) mbar_expect_tx(&S.full[st], bytes * kVCols);
       __syncwarp();
 #pragma unroll
@@ -341,8 +349,8 @@ __device__ __forceinline__ void gu_cta(const GuArgs &a, int c, int k, VpSmem &S)
       const int st = cc % kVStages;
       mbar_wait(&S.full[st], (uint32_t)((cc / kVStages) & 1));
       double *buf = &S.ring[st][0][0];
-      const int64_t r = r0 + (int64_t)cc * kRch;
-      const int nr = (int)min64(kRch, r1 - r);
+      const int64_t r = r0 + (int64_t)cc * kVRch;
+      const int nr = (int)min64(kVRch, r1 - r);
       if (mine) {
         vp_transform(buf, 32 * h, 32 * h + 16, bf, 0xFu, 0xFu, a.G, a.ldg, gcol, r, nr, g, t);
         fence_async_smem_cta();
@@ -379,8 +387,8 @@ __device__ __forceinline__ void gu_cta(const GuArgs &a, int c, int k, VpSmem &S)
   for (int cc = 0; cc < nchunk; cc++) {
     const int st = cc % kVStages;
     mbar_wait(&S.adone[st], (uint32_t)((cc / kVStages) & 1));
-    const int64_t r = r0 + (int64_t)cc * kRch;
-    const int nr = (int)min64(kRch, r1 - r);
+    const int64_t r = r0 + (int64_t)cc * kVRch;
+    const int nr = (int)min64(kVRch, r1 - r);
     gu_gram_tiles(&S.ring[st][0][0], nr, cb, acc, g, t);
     __syncwarp();
     if (lane == 0) mbar_arrive(&S.empty[st]);
