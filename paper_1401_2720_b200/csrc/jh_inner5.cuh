@@ -12,6 +12,25 @@
 #ifndef JH_I5_ROLLED
 #define JH_I5_ROLLED 1
 #endif
+// JH_I5_PROF=1 builds K2 variant 5 with clock64 phase stamps of thread 0
+// (jh_inner5_profile; dev builds only, tools/build_variant.sh)
+#ifndef JH_I5_PROF
+#define JH_I5_PROF 0
+#endif
+#if JH_I5_PROF
+#define I5_LAP(acc)                            \
+  do {                                         \
+    if (tid == 0) {                            \
+      const long long now_ = clock64();        \
+      acc += (unsigned long long)(now_ - t5_); \
+      t5_ = now_;                              \
+    }                                          \
+  } while (0)
+#else
+#define I5_LAP(acc) \
+  do {              \
+  } while (0)
+#endif
 
 namespace jh {
 
@@ -177,6 +196,42 @@ __device__ __forceinline__ void rot_apply_rows(double *M, int ld, const int8_t *
   }
 }
 
+// Rotations of one inner p-step applied to M by all NTH threads, one pair
+// per NTH / HALF threads: thread (pair, sub) rotates rows sub, sub + NTH /
+// HALF, ... of its pair's two columns, all loads before the stores (same
+// arithmetic as rot_apply5; one parameter fetch per thread).
+template <int W, int HALF, int NTH>
+__device__ __forceinline__ void rot_apply_pair(double *M, int ld, const int8_t *pst,
+                                               const StepParams5 *prm, int tid) {
+  constexpr int TPP = NTH / HALF;  // threads per pair
+  constexpr int RPT = W / TPP;     // rows per thread
+  static_assert(NTH % HALF == 0 && W % TPP == 0, "apply layout");
+  const int pi = tid / TPP, sub = tid - pi * TPP;
+  const StepParams5 P = prm[pi];
+  if (!P.act) return;
+  const int cp = pst[2 * pi], cq = pst[2 * pi + 1];
+  double *mp = M + cp * ld + sub, *mq = M + cq * ld + sub;
+  double vp[RPT], vq[RPT];
+#pragma unroll
+  for (int u = 0; u < RPT; u++) {
+    vp[u] = mp[u * TPP];
+    vq[u] = mq[u * TPP];
+  }
+  const double cs = P.cs, tn = P.tn;
+  const double sn = (P.act & 4) ? tn : -tn;
+  const bool sw = (P.act & 3) == 2;
+#pragma unroll
+  for (int u = 0; u < RPT; u++) {
+    double np = fma(sn, vq[u], vp[u]), nq = fma(tn, vp[u], vq[u]);
+    if (cs != 1.0) {
+      np = np * cs;
+      nq = nq * cs;
+    }
+    mp[u * TPP] = sw ? nq : np;
+    mq[u * TPP] = sw ? np : nq;
+  }
+}
+
 // Returns the task's rotation count (>= 0, V' written to Vg column-major,
 // counters updated) or -1 after recording a numerical failure under key
 // (pstep, task_key).  smem must hold an InnerSmem5<W>.  All NTH threads call.
@@ -273,6 +328,11 @@ __device__ __noinline__ long long inner5_task(unsigned char *smem, const double 
   int64_t tot_rot = 0, tot_proper = 0;
   int sweeps = 0, status = 0, bad = -1;
   int gstep = 0;  // global inner p-step counter (for the lagged V update)
+#if JH_I5_PROF
+  long long t5_ = clock64();
+  unsigned long long p5_dots = 0, p5_rot = 0, p5_bar1 = 0, p5_app = 0;
+  const long long t5_task = t5_;
+#endif
   const int ri = tid % W;         // row handled in the R / V applies
   const int rg = tid / W;         // pair group
   constexpr int RGS = NTH / W;    // pair groups in the R apply
@@ -297,6 +357,10 @@ __device__ __noinline__ long long inner5_task(unsigned char *smem, const double 
           // the rotation is formed speculatively, in parallel with the
           // orthogonality test (it has no side effects; a pair that passes
           // the test discards it, exactly like the reference never forms it)
+#if JH_I5_PROF
+          asm volatile("" ::"d"(hpp), "d"(hqq), "d"(hpq));
+#endif
+          I5_LAP(p5_dots);
           const bool hyp = S.sg[p] > 0 && S.sg[q] < 0;
           // branch-free fast paths of the IEEE division / square root
           // (jh_fastmath.cuh; the IEEE operators when an operand leaves
@@ -335,6 +399,7 @@ __device__ __noinline__ long long inner5_task(unsigned char *smem, const double 
             }
           }
           cur[lane] = pr;
+          I5_LAP(p5_rot);
         }
         const unsigned fm = __ballot_sync(0xffffffffu, fail != 0);
         if (fm) {
@@ -358,6 +423,7 @@ __device__ __noinline__ long long inner5_task(unsigned char *smem, const double 
             if (prev[pi].act) rot_apply5(S.V, LD, pst[2 * pi], pst[2 * pi + 1], vrow, prev[pi]);
       }
       __syncthreads();
+      I5_LAP(p5_bar1);
       if (S.stop) {
         status = S.fail_status;
         bad = S.fail_bad;
@@ -366,13 +432,16 @@ __device__ __noinline__ long long inner5_task(unsigned char *smem, const double 
       // R update of this inner p-step (all threads); the per-pair loop
       // (JH_I5_ROLLED, default) keeps K2 at 104 registers and measured as
       // fast as the batched form at n = 16384 (275 vs 285 us per launch)
-#if JH_I5_ROLLED
+#if JH_I5_ROLLED == 2
       for (int pi = rg; pi < HALF; pi += RGS)
         if (cur[pi].act) rot_apply5(S.R, LD, st[2 * pi], st[2 * pi + 1], ri, cur[pi]);
+#elif JH_I5_ROLLED == 1
+      rot_apply_pair<W, HALF, NTH>(S.R, LD, st, cur, tid);
 #else
       rot_apply_rows<HALF, RGS>(S.R, LD, st, cur, rg, ri);
 #endif
       __syncthreads();
+      I5_LAP(p5_app);
     }
     if (status) break;
     // sweep end: totals of applied / proper rotations
@@ -412,6 +481,18 @@ __device__ __noinline__ long long inner5_task(unsigned char *smem, const double 
     const int j = e / W, i = e - j * W;
     Vg[e] = S.V[j * LD + i];
   }
+#if JH_I5_PROF
+  if (tid == 0 && g_i5_on) {
+    atomicAdd(&g_i5[1], p5_dots);
+    atomicAdd(&g_i5[2], p5_rot);
+    atomicAdd(&g_i5[3], p5_bar1);
+    atomicAdd(&g_i5[4], p5_app);
+    atomicAdd(&g_i5[5], (unsigned long long)gstep);
+    atomicAdd(&g_i5[6], (unsigned long long)sweeps);
+    atomicAdd(&g_i5[7], 1ull);
+    atomicAdd(&g_i5[8], (unsigned long long)(clock64() - t5_task));
+  }
+#endif
   if (tid == 0) {
     *rot_out = tot_rot;
     atomicAdd(&counters[0], (unsigned long long)tot_rot);
