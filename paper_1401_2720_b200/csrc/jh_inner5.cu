@@ -6,6 +6,7 @@
 // (JHSVD_INNER=3/4).
 #include "jh_inner5.cuh"
 #include "jh_inner6.cuh"
+#include "jh_inner7.cuh"
 #include "jh_kernels.h"
 
 namespace jh {
@@ -75,7 +76,46 @@ k_factor_inner6(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
   }
 }
 
+// Variant 7 (jh_inner7.cuh): one barrier per inner p-step, stored-R and V
+// updates off warp 0's chain (w <= 32; opt-in JHSVD_I7=1: bitwise equal but
+// slower, 368 vs 254 us per launch at n = 16384 -- the on-the-fly columns and
+// the per-row shuffles lengthen warp 0's chain more than the barrier saves).
+template <int W>
+__global__ void __launch_bounds__(InnerCfg5<W>::NTH, 4)
+k_factor_inner7(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
+                int64_t *__restrict__ task_rot, const int32_t *__restrict__ pairs,
+                int64_t n_plus, const int32_t *__restrict__ inner, int inner_limit,
+                double tol_c, unsigned long long *counters, int pstep, bool from_r,
+                int64_t *done, int64_t epoch) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int task = blockIdx.x;
+  inner7_task<W, InnerCfg5<W>::NTH>(smraw, Hbuf + (size_t)task * W * W, Vbuf + (size_t)task * W * W,
+                                    pairs[2 * task], pairs[2 * task + 1], n_plus, inner,
+                                    inner_limit, tol_c, counters, pstep, task, &task_rot[task],
+                                    from_r);
+  if (done) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(done + task), "l"(epoch) : "memory");
+      int64_t *rl = done + gridDim.x;
+      const unsigned long long k = atomicAdd((unsigned long long *)rl, 1ull);
+      asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(rl + 1 + k),
+                   "l"((epoch << 24) | task) : "memory");
+    }
+  }
+}
+
 bool inner5_ok(int w) { return w == 16 || w == 32 || w == 64; }
+
+static bool use_inner7(int w) {
+  static const bool on = [] {
+    const char *e = getenv("JHSVD_I7");
+    return e && e[0] == '1';
+  }();
+  return on && w <= 32;
+}
 
 static bool use_inner6(int w) {
   static const bool on = [] {
@@ -91,6 +131,19 @@ static void launch_inner5_t(const double *Hbuf, double *Vbuf, int64_t *trot, con
                            double tol_c, unsigned long long *counters, int pstep,
                            cudaStream_t st, bool from_r, int64_t *done, int64_t epoch) {
   if constexpr (W <= 32) {
+    if (use_inner7(W) && !use_inner6(W)) {
+      const size_t smem7 = sizeof(InnerSmem7<W>);
+      static bool attr7 = false;
+      if (!attr7) {
+        cudaFuncSetAttribute(k_factor_inner7<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem7);
+        attr7 = true;
+      }
+      k_factor_inner7<W><<<ntask, InnerCfg5<W>::NTH, smem7, st>>>(
+          Hbuf, Vbuf, trot, pairs, n_plus, inner, inner_limit, tol_c, counters, pstep, from_r,
+          done, epoch);
+      return;
+    }
     if (use_inner6(W)) {
       const size_t smem6 = sizeof(InnerSmem6<W>);
       static bool attr6 = false;

@@ -199,11 +199,12 @@ def test_dmma_probe_runs():
 
 
 @pytest.mark.parametrize("env", [{"JHSVD_I6": "1"}, {"JHSVD_ENGINE": "0", "JHSVD_I6": "1"},
+                                 {"JHSVD_I7": "1"}, {"JHSVD_ENGINE": "0", "JHSVD_I7": "1"},
                                  {"JHSVD_GMIX": "0"}, {"JHSVD_GMIX": "1"}])
 def test_kernel_variants_bitwise_in_subprocess(env, solves_golden):
     """Opt-in kernel variants (read once per process from the environment)
-    give the reference golden bitwise: inner variant 6, Grams in the update
-    launch on / off."""
+    give the reference golden bitwise: inner variants 6 and 7, Grams in the
+    update launch on / off."""
     import json
     import os
     import subprocess
