@@ -371,7 +371,8 @@ __device__ __noinline__ long long inner5_task(unsigned char *smem, const double 
           bool rot_ok = rotation_core_fast(hpp, hqq, hpq, hyp ? -1.0 : 1.0, cs, tn, sp, sq,
                                            fast_ok);
           if (!fast_ok) {
-            rot_ok = rotation_core(hpp, hqq, hpq, hyp ? -1.0 : 1.0, cs, tn);
+            // out of the fast paths' range (e.g. hpq == 0): IEEE operators,
+            // the rotation only when the pair is rotated
             sp = sqrt(hpp);
             sq = sqrt(hqq);
           }
@@ -382,6 +383,7 @@ __device__ __noinline__ long long inner5_task(unsigned char *smem, const double 
             fail = kZeroColumn;
             fb = q + 1;
           } else if (!(fabs(hpq) < tol_c * sp * sq)) {
+            if (!fast_ok) rot_ok = rotation_core(hpp, hqq, hpq, hyp ? -1.0 : 1.0, cs, tn);
             if (!rot_ok) {
               fail = kHypDomain;
               fb = p + 1;
