@@ -454,11 +454,13 @@ __device__ __forceinline__ int tagged_inc(int64_t *p, int64_t epoch) {
 __device__ __forceinline__ void gram_cta32(const double *G, int64_t ldg, int64_t m, int p, int q,
                                            double *H, double *sm, uint64_t *full,
                                            uint64_t *empty) {
+  // the G-item ring of the launch: kMixGStages x 32 columns x (kMixGRch + 4)
   constexpr int W = 32, NW = 4, BW = 16, MY = GramTiles<W, NW>::MY;
+  constexpr int RCH = kMixGRch, LD = kMixGRch + 4, STG = kMixGStages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const int64_t nchunk = cdiv(m, kRch);
+  const int64_t nchunk = cdiv(m, RCH);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; s++) {
+    for (int s = 0; s < STG; s++) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NW);
     }
@@ -469,14 +471,14 @@ __device__ __forceinline__ void gram_cta32(const double *G, int64_t ldg, int64_t
   if (warp == 0) {
     fence_async_global();  // the block-columns were just written by generic stores
     for (int64_t c = 0; c < nchunk; c++) {
-      const int s = (int)(c % kStages);
-      if (c >= kStages) mbar_wait(&empty[s], (uint32_t)(((c / kStages) - 1) & 1));
-      const int64_t r0 = c * kRch;
-      const uint32_t bytes = (uint32_t)min64(kRch, m - r0) * 8u;
+      const int s = (int)(c % STG);
+      if (c >= STG) mbar_wait(&empty[s], (uint32_t)(((c / STG) - 1) & 1));
+      const int64_t r0 = c * RCH;
+      const uint32_t bytes = (uint32_t)min64(RCH, m - r0) * 8u;
       if (lane == 0) mbar_expect_tx(&full[s], bytes * W);
       __syncwarp();
       const int64_t col = lane < BW ? (int64_t)p * BW + lane : (int64_t)q * BW + (lane - BW);
-      bulk_g2s(sm + ((size_t)s * W + lane) * kLd, G + col * ldg + r0, bytes, &full[s]);
+      bulk_g2s(sm + ((size_t)s * W + lane) * LD, G + col * ldg + r0, bytes, &full[s]);
     }
     return;
   }
@@ -485,15 +487,15 @@ __device__ __forceinline__ void gram_cta32(const double *G, int64_t ldg, int64_t
 #pragma unroll
   for (int i = 0; i < MY; i++) acc[i][0] = acc[i][1] = 0.0;
   for (int64_t c = 0; c < nchunk; c++) {
-    const int s = (int)(c % kStages);
-    mbar_wait(&full[s], (uint32_t)((c / kStages) & 1));
-    const double *buf = sm + (size_t)s * W * kLd + (size_t)g * kLd + t;
-    const int nr = (int)min64(kRch, m - c * kRch);
+    const int s = (int)(c % STG);
+    mbar_wait(&full[s], (uint32_t)((c / STG) & 1));
+    const double *buf = sm + (size_t)s * W * LD + (size_t)g * LD + t;
+    const int nr = (int)min64(RCH, m - c * RCH);
     switch (cw) {
-      case 0: gram_chunk<W, NW, 0>(buf, nr, acc, t); break;
-      case 1: gram_chunk<W, NW, 1>(buf, nr, acc, t); break;
-      case 2: gram_chunk<W, NW, 2>(buf, nr, acc, t); break;
-      default: gram_chunk<W, NW, 3>(buf, nr, acc, t); break;
+      case 0: gram_chunk<W, NW, 0, RCH>(buf, nr, acc, t); break;
+      case 1: gram_chunk<W, NW, 1, RCH>(buf, nr, acc, t); break;
+      case 2: gram_chunk<W, NW, 2, RCH>(buf, nr, acc, t); break;
+      default: gram_chunk<W, NW, 3, RCH>(buf, nr, acc, t); break;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
