@@ -917,15 +917,15 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
   // Grams of p-step s+1 as trailing CTAs of the update launch of p-step s
   // (each starts when the G slabs of the two tasks that wrote its
   // block-columns are done), so the Gram pass overlaps the update's tail
-  // JHSVD_GMIX=1 / 0 forces it on / off; by default on from 256 tasks per
-  // p-step for G of at most 2^26 entries (n = 8192: 0.650 vs 0.662 ms per
-  // p-step); slower for larger G (16384^2: 2.16 vs 2.07) and for 128 tasks
-  // (config 2: 0.443 vs 0.429 s), profiles/r01/cycle_engine.md
+  // JHSVD_GMIX=1 / 0 forces it on / off; by default on for G of at most
+  // 2^26 entries (n = 8192: 0.626 vs 0.649 ms per p-step, config 2: 0.414
+  // vs 0.428 s); slower for larger G (16384^2: 1.86 vs 1.83 ms per p-step),
+  // profiles/r01/cycle_engine.md
   static const int gmix_env = [] {
     const char *e = getenv("JHSVD_GMIX");
     return e ? (e[0] == '1' ? 1 : 0) : -1;
   }();
-  const bool gmix = (gmix_env == 1 || (gmix_env < 0 && ntask >= 256 && m * n <= (int64_t(1) << 26))) && !gu && !separate &&
+  const bool gmix = (gmix_env == 1 || (gmix_env < 0 && m * n <= (int64_t(1) << 26))) && !gu && !separate &&
                     w == 32 && nsteps > 1;
   if (gmix) {
     cudaMemsetAsync(gcnt, 0, sizeof(int64_t) * ntask, st);
