@@ -14,6 +14,9 @@
 #endif
 // JH_I5_PROF=1 builds K2 variant 5 with clock64 phase stamps of thread 0
 // (jh_inner5_profile; dev builds only, tools/build_variant.sh)
+#ifndef JH_I5_SPLIT
+#define JH_I5_SPLIT 0
+#endif
 #ifndef JH_I5_PROF
 #define JH_I5_PROF 0
 #endif
@@ -342,8 +345,31 @@ __device__ __noinline__ long long inner5_task(unsigned char *smem, const double 
       StepParams5 *cur = S.prm[gstep & 1];
       if (warp == 0) {
         int fail = 0, fb = 0;
+#if JH_I5_SPLIT
+        // (build option, measured slower: 289 vs 259 us per launch) the three
+        // chains of pair i on two lanes: lane i runs hpp and hpq,
+        // lane i + w/2 runs hqq (same fma order; its second chain is unused)
+        double hpp, hqq, hpq;
+        {
+          const bool upper = lane >= HALF;
+          const int pl = lane < 2 * HALF ? (upper ? lane - HALF : lane) : 0;
+          const int pa = st[2 * pl + (upper ? 1 : 0)], pb = st[2 * pl + (upper ? 0 : 1)];
+          const double *ca = S.R + pa * LD, *cb = S.R + pb * LD;
+          double a1 = 0.0, a2 = 0.0;
+#pragma unroll
+          for (int i = 0; i < W; i++) {
+            const double x = ca[i], y = cb[i];
+            a1 = fma(x, x, a1);
+            a2 = fma(x, y, a2);
+          }
+          hpp = a1;
+          hpq = a2;
+          hqq = __shfl_down_sync(0xffffffffu, a1, HALF);
+        }
+#endif
         if (lane < HALF) {
           const int p = st[2 * lane], q = st[2 * lane + 1];
+#if !JH_I5_SPLIT
           const double *cp = S.R + p * LD, *cq = S.R + q * LD;
           double hpp = 0.0, hqq = 0.0, hpq = 0.0;
 #pragma unroll
@@ -353,6 +379,7 @@ __device__ __noinline__ long long inner5_task(unsigned char *smem, const double 
             hqq = fma(gq, gq, hqq);
             hpq = fma(gp, gq, hpq);
           }
+#endif
           StepParams5 pr{1.0, 0.0, 0};
           // the rotation is formed speculatively, in parallel with the
           // orthogonality test (it has no side effects; a pair that passes
