@@ -14,6 +14,9 @@
 #endif
 // JH_I5_PROF=1 builds K2 variant 5 with clock64 phase stamps of thread 0
 // (jh_inner5_profile; dev builds only, tools/build_variant.sh)
+#ifndef JH_I5_DOTU
+#define JH_I5_DOTU 32  // unroll of the dot-product loop
+#endif
 #ifndef JH_I5_SPLIT
 #define JH_I5_SPLIT 0
 #endif
@@ -36,6 +39,8 @@
 #endif
 
 namespace jh {
+
+constexpr int kI5DotUnroll = JH_I5_DOTU;
 
 // IEEE a / b and sqrt(x) through the branch-free fast paths when they are in
 // range (bitwise the same values), the operators otherwise
@@ -372,7 +377,7 @@ __device__ __noinline__ long long inner5_task(unsigned char *smem, const double 
 #if !JH_I5_SPLIT
           const double *cp = S.R + p * LD, *cq = S.R + q * LD;
           double hpp = 0.0, hqq = 0.0, hpq = 0.0;
-#pragma unroll
+#pragma unroll kI5DotUnroll
           for (int i = 0; i < W; i++) {
             const double gp = cp[i], gq = cq[i];
             hpp = fma(gp, gp, hpp);
