@@ -36,8 +36,17 @@ __device__ __forceinline__ double ld_f64(const double *p) {
   return v;
 }
 
+#ifndef JH_STG_MODE
+#define JH_STG_MODE 0
+#endif
 __device__ __forceinline__ void st_f64(double *p, double v) {
+#if JH_STG_MODE == 1
+  __stcs(p, v);  // streaming store, schedulable like any store
+#elif JH_STG_MODE == 2
+  *p = v;
+#else
   asm volatile("st.global.L1::no_allocate.f64 [%0], %1;" ::"l"(p), "d"(v));
+#endif
 }
 
 // ---- mbarrier + bulk async copy (TMA engine, SASS UBLKCP) -----------------
