@@ -159,3 +159,33 @@ def test_engine_reports_first_failure_like_pstep_path(engine):
     k1 = eng.sweep(G1, V1).clone().tolist()
     k2 = ref.sweep(G2, V2).clone().tolist()
     assert k1[2] == k2[2] and k1[2] != -1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [12288, 16384])
+def test_large_prefix_bitwise_vs_oracle(n, oracle):
+    """The first p-steps at sizes whose Gram ring shape (3 or 4 CTAs per SM),
+    row slabs (4096 / 1536 rows) and mixed launch differ from the small
+    cases: G and V bitwise equal to the C oracle."""
+    import torch
+
+    from paper_1401_2720_b200.driver import SolverConfig, SweepEngine
+
+    torch.cuda.set_device(0)
+    w, steps = 32, 3
+    cfg = SolverConfig(block_width=w)
+    outer = make_strategy("rrow", n // (w // 2))
+    inner = make_strategy("rrow", w)
+    gen = torch.Generator(device="cuda").manual_seed(n)
+    G = torch.randn(n, n, dtype=torch.float64, device="cuda", generator=gen)  # rows = columns
+    host = G.cpu().numpy()
+    V = torch.eye(n, dtype=torch.float64, device="cuda")
+    eng = SweepEngine(n, n, n, cfg, outer, inner, n)
+    eng.sweep(G, V, 0, steps)
+    torch.cuda.synchronize()
+    g = np.array(host, copy=True).T  # F-order m x n
+    v = np.asfortranarray(np.eye(n))
+    oracle.block_sweep(g, v, n, dict(block_width=w, variant="full-block"),
+                       as_table(outer)[:steps], as_table(inner), threads=oracle.max_threads())
+    assert np.array_equal(G.cpu().numpy(), np.ascontiguousarray(g.T))
+    assert np.array_equal(V.cpu().numpy(), np.ascontiguousarray(v.T))
