@@ -189,3 +189,32 @@ def test_large_prefix_bitwise_vs_oracle(n, oracle):
                        as_table(outer)[:steps], as_table(inner), threads=oracle.max_threads())
     assert np.array_equal(G.cpu().numpy(), np.ascontiguousarray(g.T))
     assert np.array_equal(V.cpu().numpy(), np.ascontiguousarray(v.T))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n,steps", [(1000, 512, 5), (2050, 1024, 4)])
+def test_ragged_rows_prefix_bitwise_vs_oracle(m, n, steps, oracle):
+    """Row counts that are not multiples of the 104/128-row chunks or of the
+    row slabs: the first p-steps of the default engine against the C oracle."""
+    import torch
+
+    from paper_1401_2720_b200.driver import SolverConfig, SweepEngine
+
+    torch.cuda.set_device(0)
+    w = 32
+    cfg = SolverConfig(block_width=w)
+    outer = make_strategy("rrow", n // (w // 2))
+    inner = make_strategy("rrow", w)
+    gen = torch.Generator(device="cuda").manual_seed(m + n)
+    G = torch.randn(n, m, dtype=torch.float64, device="cuda", generator=gen)  # rows = columns
+    host = G.cpu().numpy()
+    V = torch.eye(n, dtype=torch.float64, device="cuda")
+    eng = SweepEngine(m, n, n, cfg, outer, inner, n)
+    eng.sweep(G, V, 0, steps)
+    torch.cuda.synchronize()
+    g = np.array(host, copy=True).T  # F-order m x n
+    v = np.asfortranarray(np.eye(n))
+    oracle.block_sweep(g, v, n, dict(block_width=w, variant="full-block"),
+                       as_table(outer)[:steps], as_table(inner), threads=oracle.max_threads())
+    assert np.array_equal(G.cpu().numpy(), np.ascontiguousarray(g.T))
+    assert np.array_equal(V.cpu().numpy(), np.ascontiguousarray(v.T))
