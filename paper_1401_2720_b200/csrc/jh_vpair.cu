@@ -76,8 +76,14 @@ constexpr int kMixGRch = JH_MGRCH;  // rows per G-item chunk
 #define JH_VORDER 0
 #endif
 constexpr int kMixVOrder = JH_VORDER;  // ring stages of the G items (the union with the V ring)
-constexpr int kMixGSlab[2] = {2048, 4096};
-constexpr int kMixVSlab[2] = {512, 1536};
+#ifndef JH_GBIG
+#define JH_GBIG 4096
+#endif
+#ifndef JH_VBIG
+#define JH_VBIG 1536
+#endif
+constexpr int kMixGSlab[2] = {2048, JH_GBIG};
+constexpr int kMixVSlab[2] = {512, JH_VBIG};
 
 struct VpSmem {
   double ring[kVStages][kVCols][kVLd];
