@@ -1,3 +1,4 @@
+#include <atomic>
 // The p-step of the blocked one-sided Jacobi (H)SVD on one B200.
 //
 // Reference: run_block_jacobi_inplace / task (pkg/src/jhsvd/driver.py:125-200)
@@ -901,7 +902,10 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
   // dependent launch + per-task flags); JHSVD_PDL=0 or jh_set_overlap(0)
   // disables (per-kernel timing needs the kernels apart)
   const bool pdl = g_overlap;
-  static int64_t epoch = 0;
+  // release-flag epochs: process-wide and atomic, so that solves issued from
+  // several host threads never share one
+  static std::atomic<int64_t> epoch_ctr{0};
+  int64_t epoch = 0;
   if (pdl && !separate) cudaMemsetAsync(done, 0xff, sizeof(int64_t) * (2 * ntask + 1), st);
   // opt-in (JHSVD_GU=1): the update launch of p-step s also forms the
   // Grams of p-step s+1 (one pass over G per p-step, Gram chains handed
@@ -942,7 +946,7 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
     }
     const bool use_pdl = pdl && !separate;
     if (use_pdl) {
-      epoch++;
+      epoch = ++epoch_ctr;
       cudaMemsetAsync(done + ntask, 0, sizeof(int64_t), st);  // ready-list count
     }
     // (with the programmatic launch, class 1 times the inner Jacobi and the

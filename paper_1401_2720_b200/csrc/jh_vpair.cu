@@ -1,3 +1,4 @@
+#include <atomic>
 // V update of a pair of p-steps in one pass over V (engine 1).
 //
 // V is read by nothing else until the sweep ends, so the post-multiplication
@@ -712,7 +713,7 @@ void launch_update_mix(double *G, int64_t ldg, int64_t m, const int32_t *pairs, 
   a.nG = ntask * a.nslab_g;
   if (Hnext) {
     // G update fused with the Grams of the next p-step
-    static int64_t sepoch = 0;
+    static std::atomic<int64_t> sepoch{0};
     GuArgs &u = a.gu;
     a.use_gu = 1;
     u.G = G;
@@ -764,7 +765,7 @@ void launch_update_mix(double *G, int64_t ldg, int64_t m, const int32_t *pairs, 
     a.nsrc++;
   }
   if (pairs_next && m > 0) {
-    static int64_t gepoch = 0;
+    static std::atomic<int64_t> gepoch{0};
     a.nGr = ntask;
     a.pairs_next = pairs_next;
     a.colpos = colpos;
