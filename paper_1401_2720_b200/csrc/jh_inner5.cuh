@@ -17,6 +17,9 @@
 #ifndef JH_I5_DOTU
 #define JH_I5_DOTU 32  // unroll of the dot-product loop
 #endif
+#ifndef JH_I5_PREF
+#define JH_I5_PREF 1
+#endif
 #ifndef JH_I5_SPLIT
 #define JH_I5_SPLIT 0
 #endif
@@ -344,6 +347,13 @@ __device__ __noinline__ long long inner5_task(unsigned char *smem, const double 
   const int ri = tid % W;         // row handled in the R / V applies
   const int rg = tid / W;         // pair group
   constexpr int RGS = NTH / W;    // pair groups in the R apply
+  // pair of warp-0 lane i in the next inner p-step, loaded one step ahead
+  // (the table is read-only; JH_I5_PREF=0 loads it in the step)
+  int p_next = 0, q_next = 0;
+  if (JH_I5_PREF && warp == 0 && lane < HALF) {
+    p_next = S.steps[2 * lane];
+    q_next = S.steps[2 * lane + 1];
+  }
   for (int sw = 0; sw < inner_limit && !status; sw++) {
     for (int si = 0; si < NSTEP; si++, gstep++) {
       const int8_t *st = S.steps + si * W;
@@ -373,7 +383,16 @@ __device__ __noinline__ long long inner5_task(unsigned char *smem, const double 
         }
 #endif
         if (lane < HALF) {
+#if JH_I5_PREF
+          const int p = p_next, q = q_next;
+          {
+            const int8_t *stn = S.steps + (si + 1 < NSTEP ? si + 1 : 0) * W;
+            p_next = stn[2 * lane];
+            q_next = stn[2 * lane + 1];
+          }
+#else
           const int p = st[2 * lane], q = st[2 * lane + 1];
+#endif
 #if !JH_I5_SPLIT
           const double *cp = S.R + p * LD, *cq = S.R + q * LD;
           double hpp = 0.0, hqq = 0.0, hpq = 0.0;
