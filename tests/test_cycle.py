@@ -162,7 +162,7 @@ def test_engine_reports_first_failure_like_pstep_path(engine):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n", [12288, 16384])
+@pytest.mark.parametrize("n", [8192, 12288, 16384])
 def test_large_prefix_bitwise_vs_oracle(n, oracle):
     """The first p-steps at sizes whose Gram ring shape (3 or 4 CTAs per SM),
     row slabs (4096 / 1536 rows) and mixed launch differ from the small
@@ -218,3 +218,26 @@ def test_ragged_rows_prefix_bitwise_vs_oracle(m, n, steps, oracle):
                        as_table(outer)[:steps], as_table(inner), threads=oracle.max_threads())
     assert np.array_equal(G.cpu().numpy(), np.ascontiguousarray(g.T))
     assert np.array_equal(V.cpu().numpy(), np.ascontiguousarray(v.T))
+
+
+@pytest.mark.gpu
+def test_full_solve_4096_bitwise_vs_oracle(oracle):
+    """A whole solve at n = 4096 (128 tasks per p-step: the 2-per-SM Gram
+    ring, short slabs, the Grams of the next p-step inside the update
+    launch) bitwise equal to the C oracle: stats, sigma, U and V."""
+    import torch
+
+    import paper_1401_2720_b200 as J
+
+    torch.cuda.set_device(0)
+    n = 4096
+    rng = np.random.default_rng(11)
+    g = np.asfortranarray(rng.standard_normal((n, n)))
+    cfg = J.SolverConfig(block_width=32)
+    res = J.block_jacobi(g, None, cfg)
+    outer = J.as_table(J.make_strategy("rrow", n // 16))
+    inner = J.as_table(J.make_strategy("rrow", 32))
+    ref = oracle.block_jacobi(g, n, cfg, outer, inner, threads=oracle.max_threads())
+    assert res.stats == ref.stats
+    assert np.array_equal(res.sigma, ref.sigma)
+    assert np.array_equal(res.u, ref.u) and np.array_equal(res.v, ref.v)
