@@ -2,6 +2,7 @@
 (run once on a GPU box; minutes of oracle time):
     python tools/validate_full.py 4   -> config 4 (8192 HSVD, n/2 negative)
     python tools/validate_full.py 2   -> config 2 (4096 graded, block-oriented)
+    python tools/validate_full.py 3   -> config 3 (16384, the bench input; ~80 min of oracle)
 Prints one JSON line."""
 import hashlib
 import json
@@ -26,7 +27,15 @@ def sha(a):
 
 def main():
     which = int(sys.argv[1]) if len(sys.argv) > 1 else 4
-    if which == 4:
+    if which == 3:
+        n = 16384
+        lam = T.gen_spectrum(T.SpectrumSpec(2, n, 3))
+        lam_sorted, n_plus = T.canonical_sort(lam)
+        G0 = T.gen_factor_orth_device(np.sqrt(np.abs(lam_sorted)), seed=3)
+        g = np.asfortranarray(G0.cpu().numpy().T)
+        del G0
+        cfg = J.SolverConfig(block_width=32)
+    elif which == 4:
         n = 8192
         rng = np.random.default_rng(4)
         k = max(n / 1024.0, 1.0)
