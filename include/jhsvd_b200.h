@@ -32,64 +32,64 @@
 extern "C" {
 #endif
 
-/* Device workspace for jh_block_sweep at order n and block width w. */
-int64_t jh_sweep_workspace_bytes(int64_t n, int w);
+/*
+ * Device workspace of jh_block_sweep at order n, block width w, for a pivot
+ * table of `steps` p-steps (<= 0: the full b - 1 of one block sweep);
+ * -1 for an invalid width.
+ */
+int64_t jh_sweep_workspace_bytes(int64_t n, int w, int64_t steps);
 
 /*
- * p-steps [first_step, first_step + nsteps) of one block sweep of
- * run_block_jacobi_inplace (reference driver.py:125-200, task :153-174):
- * per task Gram (blockkernel.py:76-107), Cholesky (:110-145), inner
- * pointwise Jacobi (:278-400), and -- when the task rotated -- the
+ * 4-cycle plan of a host pivot table int32[steps][b/2][2] (0-based): 0 when
+ * every pair of consecutive p-steps pairs the block-columns in 4-cycles
+ * (rrow, the Mantharam-Eberlein equivalent), so engine 1 can update V once
+ * per two p-steps; 1 otherwise.  plan has jh_cycle_plan_ints(b, steps)
+ * entries; jh_block_sweep reads the device copy.
+ */
+int64_t jh_cycle_plan_ints(int b, int steps);
+int jh_cycle_plan(const int32_t *outer, int b, int steps, int32_t *plan);
+
+/*
+ * p-steps [first_step, first_step + nsteps) of the pivot table `outer`
+ * (device int32[outer_steps][b/2][2], 0-based block-columns, b = n/(w/2)):
+ * the sweep loop body of run_block_jacobi_inplace (reference
+ * driver.py:180-190) -- per task (driver.py:153-174) the Gram
+ * (blockkernel.py:76-107) and Cholesky (:110-145) or, with shortening = 1,
+ * the QR peel-off (:148-244; w in {16, 32}, m % w == 0), the inner
+ * pointwise Jacobi (:278-400) and, when the task rotated, the
  * post-multiplication of [Gp Gq] and [Vp Vq] (:407-428).
- *   G  m x n (ld ldg), V nv x n (ld ldv) or NULL; updated in place.
- *   w  block width (shortened order), even, 2 <= w <= 64, n % w == 0.
+ *   G      m x n (ld ldg), updated in place;
+ *   V      nv x n (ld ldv) or NULL, updated in place;
+ *   w      block width (shortened order), even, 2 <= w <= 64, n % w == 0;
+ *   plan   device copy of jh_cycle_plan for `outer` or NULL;
+ *   gblock NULL, or device int32[b]: the global block-column index of each
+ *          local block-column (sharded solves; the J signature of a column
+ *          follows its global index, column j of the factor is + iff
+ *          j < n_plus);
+ *   engine 0 per-p-step kernels; 1 the same G path with V updated once per
+ *          two p-steps inside the G update launches (needs V, w = 32 and
+ *          plan; otherwise engine 0).  Both give bitwise the same results.
  *   counters: uint64[4] device: [0] += rotations, [1] += proper rotations,
  *     [2] = min error key (initialise to UINT64_MAX), [3] += tasks that
- *     rotated (their pair columns were post-multiplied); key layout
- *     p-step<<38 | task<<16 | status<<13 | 1-based index, status 1 =
- *     Cholesky pivot, 2 = zero column, 3 = hyperbolic domain.
+ *     rotated; key = p-step<<38 | task<<16 | status<<13 | 1-based index,
+ *     status 1 = Cholesky pivot, 2 = zero column, 3 = hyperbolic domain.
  */
 int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int64_t ldv,
-                   int64_t nv, int w, const int32_t *outer, int first_step, int nsteps,
+                   int64_t nv, int w, const int32_t *outer, int outer_steps, const int32_t *plan,
+                   const int32_t *gblock, int engine, int shortening, int first_step, int nsteps,
                    const int32_t *inner, int64_t n_plus, int inner_limit, double tol_c,
                    void *workspace, int64_t ws_bytes, unsigned long long *counters,
                    void *stream);
-
-/*
- * Sweep engines for pivot tables whose consecutive p-steps pair the
- * block-columns in 4-cycles (rrow, the Mantharam-Eberlein equivalent):
- * jh_cycle_plan (host) checks the structure of a host pivot table
- * int32[b-1][b/2][2] and fills plan[jh_cycle_plan_ints(b)] (return 0 =
- * usable, 1 = not usable).  jh_block_sweep2 runs the same p-steps as
- * jh_block_sweep -- bitwise the same G, V and counters -- on
- *   engine 0: the per-p-step kernels (= jh_block_sweep),
- *   engine 1: per-p-step kernels for G; V updated once per pair of p-steps
- *             on a low-priority stream (needs V, w = 32, the device plan),
- *   engine 2: the cycle engine, one persistent kernel (needs w = 32, the
- *             device plan and jh_cycle_workspace_bytes more workspace).
- * Unsupported cases fall back to engine 0.  Same reference functions as
- * jh_block_sweep (driver.py:153-190).  shortening: 0 = Gram + Cholesky
- * (blockkernel.py:76-145), 1 = QR peel-off (blockkernel.py:148-244; per
- * p-step kernels, w in {16, 32}, m % w == 0; -1000 otherwise).
- */
-int64_t jh_cycle_plan_ints(int b);
-int jh_cycle_plan(const int32_t *outer, int b, int32_t *plan);
-int64_t jh_cycle_workspace_bytes(int64_t n, int w);
-int jh_block_sweep2(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int64_t ldv,
-                    int64_t nv, int w, const int32_t *outer, const int32_t *plan, int engine,
-                    int shortening, int first_step, int nsteps, const int32_t *inner,
-                    int64_t n_plus, int inner_limit, double tol_c, void *workspace,
-                    int64_t ws_bytes, unsigned long long *counters, void *stream);
 
 /* Engine 1: 1 (default) lets the update launch start while the inner Jacobi
  * kernel still runs (programmatic dependent launch, per-task flags); 0 keeps
  * the kernels apart (per-kernel timing).  Results are identical. */
 int jh_set_overlap(int on);
 
-/* Diagnostic: per-work-item trace of the cycle engine, records {item,
- * smid, start ns, end ns} (int64) into device buf[4 + 4 cap], buf[0] =
- * count; NULL disables. */
-int jh_cycle_trace(void *buf, int64_t cap);
+/* 1: sweeps use only the generic SIMT kernels (reference-order fma loops,
+ * any even width); 0 (default): DMMA / TMA kernels where they apply.
+ * Results are identical (tests compare the two). */
+int jh_set_simple_kernels(int on);
 
 /* gram (blockkernel.py:99-107): H = A^T A, A m x c. */
 int jh_gram(const double *A, int64_t lda, int64_t m, int c, double *H, void *stream);
@@ -136,46 +136,27 @@ int jh_check_scaling(const double *G, int64_t ldg, int64_t m, int64_t n,
 int jh_sigma_u(const double *G, int64_t ldg, int64_t m, int64_t n, double *sigma, double *U,
                int64_t ldu, unsigned long long *bad, void *stream);
 
+/*
+ * Synthetic input of the BASELINE workloads (not a reference function; the
+ * reference builds its inputs with numpy in testgen.py:82-133):
+ * G (m x n, ld ldg) = Q [diag(sigma); 0] W^T with Q, W random Givens
+ * butterflies (`passes` rounds of log2 layers) and, when n_plus = n/2, one
+ * J-orthogonal hyperbolic layer (|tanh| <= tanh_max) per round; bitwise
+ * equal to its host twin oracle/gen_butterfly.c.  m, n powers of two,
+ * m >= n, n_plus in {n, n/2}; sigma is a device array of n values.
+ * Workspace: jh_gen_workspace_bytes (-1 = unsupported shape).
+ */
+int64_t jh_gen_workspace_bytes(int64_t m, int64_t n, int64_t n_plus, int passes);
+int jh_gen_butterfly(double *G, int64_t ldg, int64_t m, int64_t n, const double *sigma,
+                     int64_t n_plus, unsigned long long seed, int passes, double tanh_max,
+                     void *workspace, int64_t ws_bytes, void *stream);
+
 /* Launch accounting / per-kernel-class timing (bench.py): classes are
- * 0 Gram, 1 factor + inner Jacobi, 2 update, 3 cycle-engine sweep kernel
+ * 0 Gram, 1 factor + inner Jacobi, 2 update, 3 V-only update launches
  * (arrays of 4).  jh_profile_end synchronizes on the recorded events. */
 unsigned long long jh_launch_count(void);
 int jh_profile_begin(int max_launches);
 int jh_profile_end(double *ms, int64_t *count);
-
-/* Diagnostic: DMMA (mma.sync m8n8k4 f64) vs in-order fma chain. */
-int jh_probe_dmma(const double *A, const double *B, const double *C, double *Dm, double *Df,
-                  int ntests, void *stream);
-
-/* Diagnostic: sustained DMMA (kind 0) / DFMA (kind 1) issue rate; each warp
- * runs 8 independent chains for `iters` iterations. */
-int jh_probe_rate(int kind, int ctas, int threads, int iters, double *out, void *stream);
-
-/* Diagnostic: inner-Jacobi phase timing (cycles of warp 0 in dots, rotation,
- * barrier, R apply, barrier; inner p-steps; inner sweeps; tasks).  on = 1
- * enables, 0 disables; out (host uint64[8]) receives and resets them. */
-int jh_inner_profile(int on, unsigned long long *out);
-// The same for the default inner kernel K2 (12 counters: cycles of thread 0
-// in load + Cholesky, dots, rotation + test, barrier 1, R apply + barrier 2;
-// inner p-steps, inner sweeps, tasks, task cycles sum, task cycles max, setup
-// cycles, Cholesky cycles; variant 6 only).
-int jh_inner5_profile(int on, unsigned long long *out);
-
-/* Diagnostic / test: branch-free division and sqrt fast paths vs the IEEE
- * operators on n operand pairs; cnt (device uint64[4]) += division
- * mismatches, division rejections, sqrt mismatches, sqrt rejections. */
-int jh_probe_fastmath(const double *a, const double *b, int64_t n, unsigned long long *cnt,
-                      void *stream);
-
-/* Diagnostic: launch inner-Jacobi kernel variant 3, 4 or 5 on the Gram
- * matrices in Hbuf (A/B timing, tools/bench_inner.py). */
-int jh_bench_inner(int variant, const double *Hbuf, double *Vbuf, int64_t *trot,
-                   const int32_t *pairs, int ntask, int w, int64_t n_plus, const int32_t *inner,
-                   int inner_limit, double tol_c, unsigned long long *counters, void *stream);
-
-/* Diagnostic: dependent-chain latencies (cycles/op) of DFMA, DMUL, division,
- * sqrt, the rotation formula and a shared-memory load; out[6]. */
-int jh_probe_latency(double *out, void *stream);
 
 #ifdef __cplusplus
 }

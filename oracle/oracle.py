@@ -65,6 +65,8 @@ def lib():
                                      _p, _i64, _i32, _d, _i32, _i32, _p, _p]
         L.or_block_sweep.restype = _i32
         L.or_max_threads.restype = _i32
+        L.or_gen_butterfly.argtypes = [_p, _i64, _i64, _i64, _p, _i64, ctypes.c_uint64, _i32, _d]
+        L.or_gen_butterfly.restype = _i32
         _lib = L
     return _lib
 
@@ -373,6 +375,20 @@ def run_distributed(g, n_plus, gw, cfg, assignments, nested_outer_tab, inner_tab
     return SimpleNamespace(sigma=sigma[order], u=np.asfortranarray(u[:, order]),
                            v=None if vf is None else np.asfortranarray(vf[:, order]),
                            stats=tuple(stats), block_sweeps=len(stats), converged=converged)
+
+
+def gen_butterfly(sigma, m=None, n_plus=None, seed=0, passes=2, tanh_max=0.1) -> np.ndarray:
+    """Host twin of the GPU input generator jh_gen_butterfly (gen_butterfly.c):
+    G = Q [diag(sigma); 0] W^T, m x n, Fortran order."""
+    sig = np.ascontiguousarray(sigma, dtype=np.float64)
+    n = sig.size
+    m = n if m is None else int(m)
+    n_plus = n if n_plus is None else int(n_plus)
+    g = np.empty((m, n), order="F")
+    rc = lib().or_gen_butterfly(_ptr(g), m, m, n, _ptr(sig), n_plus, seed, passes, tanh_max)
+    if rc:
+        raise ValueError(f"or_gen_butterfly: unsupported shape (status {rc})")
+    return g
 
 
 def max_threads() -> int:

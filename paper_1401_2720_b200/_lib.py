@@ -28,18 +28,14 @@ _c_p = ctypes.c_void_p
 
 # name -> (restype, argtypes); mirrors include/jhsvd_b200.h
 SIGNATURES = {
-    "jh_sweep_workspace_bytes": (_c_i64, [_c_i64, _c_i32]),
+    "jh_sweep_workspace_bytes": (_c_i64, [_c_i64, _c_i32, _c_i64]),
+    "jh_cycle_plan_ints": (_c_i64, [_c_i32, _c_i32]),
+    "jh_cycle_plan": (_c_i32, [_c_p, _c_i32, _c_i32, _c_p]),
     "jh_block_sweep": (_c_i32, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_i64, _c_i32,
-                                _c_p, _c_i32, _c_i32, _c_p, _c_i64, _c_i32, _c_d, _c_p, _c_i64,
-                                _c_p, _c_p]),
-    "jh_cycle_plan_ints": (_c_i64, [_c_i32]),
-    "jh_cycle_plan": (_c_i32, [_c_p, _c_i32, _c_p]),
-    "jh_cycle_workspace_bytes": (_c_i64, [_c_i64, _c_i32]),
-    "jh_block_sweep2": (_c_i32, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_i64, _c_i32,
-                                 _c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_i64,
-                                 _c_i32, _c_d, _c_p, _c_i64, _c_p, _c_p]),
-    "jh_cycle_trace": (_c_i32, [_c_p, _c_i64]),
+                                _c_p, _c_i32, _c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p,
+                                _c_i64, _c_i32, _c_d, _c_p, _c_i64, _c_p, _c_p]),
     "jh_set_overlap": (_c_i32, [_c_i32]),
+    "jh_set_simple_kernels": (_c_i32, [_c_i32]),
     "jh_gram": (_c_i32, [_c_p, _c_i64, _c_i64, _c_i32, _c_p, _c_p]),
     "jh_qr_peeloff": (_c_i32, [_c_p, _c_i64, _c_i64, _c_i32, _c_p, _c_p]),
     "jh_cholesky": (_c_i32, [_c_p, _c_i32, _c_p, _c_p, _c_p]),
@@ -50,14 +46,9 @@ SIGNATURES = {
     "jh_column_norms": (_c_i32, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p]),
     "jh_check_scaling": (_c_i32, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p]),
     "jh_sigma_u": (_c_i32, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_i64, _c_p, _c_p]),
-    "jh_probe_dmma": (_c_i32, [_c_p, _c_p, _c_p, _c_p, _c_p, _c_i32, _c_p]),
-    "jh_probe_rate": (_c_i32, [_c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_p]),
-    "jh_probe_latency": (_c_i32, [_c_p, _c_p]),
-    "jh_probe_fastmath": (_c_i32, [_c_p, _c_p, _c_i64, _c_p, _c_p]),
-    "jh_inner_profile": (_c_i32, [_c_i32, _c_p]),
-    "jh_inner5_profile": (_c_i32, [_c_i32, _c_p]),
-    "jh_bench_inner": (_c_i32, [_c_i32, _c_p, _c_p, _c_p, _c_p, _c_i32, _c_i32, _c_i64, _c_p,
-                                _c_i32, _c_d, _c_p, _c_p]),
+    "jh_gen_workspace_bytes": (_c_i64, [_c_i64, _c_i64, _c_i64, _c_i32]),
+    "jh_gen_butterfly": (_c_i32, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, ctypes.c_ulonglong,
+                                  _c_i32, _c_d, _c_p, _c_i64, _c_p]),
     "jh_launch_count": (ctypes.c_ulonglong, []),
     "jh_profile_begin": (_c_i32, [_c_i32]),
     "jh_profile_end": (_c_i32, [_c_p, _c_p]),

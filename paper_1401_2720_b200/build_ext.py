@@ -28,7 +28,6 @@ NVCC_FLAGS = [
     # exactness: never contract a*b+c; only explicit fma() rounds once
     "-fmad=false",
     "-Xcompiler", "-fPIC,-ffp-contract=off",
-    "-shared",
 ]
 
 
@@ -51,18 +50,41 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
-        return LIB
-    OUT_DIR.mkdir(exist_ok=True)
-    tmp = LIB.with_suffix(".so.tmp")
-    cmd = [_nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"), "-o", str(tmp),
-           *map(str, sources())]
+def compile_shared(srcs: list[Path], out: Path, includes: list[Path], obj_dir: Path,
+                   verbose: bool = False) -> Path:
+    """nvcc -c every source in parallel, then link one shared library."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    obj_dir.mkdir(parents=True, exist_ok=True)
+    inc = [a for d in includes for a in ("-I", str(d))]
+    nvcc = _nvcc()
+
+    def one(src: Path) -> Path:
+        obj = obj_dir / (src.stem + ".o")
+        cmd = [nvcc, *NVCC_FLAGS, *inc, "-c", "-o", str(obj), str(src)]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(one, srcs))
+    out.parent.mkdir(parents=True, exist_ok=True)
+    tmp = out.with_suffix(".so.tmp")
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp),
+           *map(str, objs)]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    if not force and not _stale():
+        return LIB
+    return compile_shared(sources(), LIB, [ROOT / "include", SRC], ROOT / "build" / "obj",
+                          verbose)
 
 
 if __name__ == "__main__":

@@ -253,7 +253,8 @@ __device__ __noinline__ long long inner5_task(unsigned char *smem, const double 
                                               int inner_limit, double tol_c,
                                               unsigned long long *counters, int pstep,
                                               int task_key, int64_t *rot_out,
-                                              bool from_r = false) {
+                                              bool from_r = false,
+                                              const int32_t *__restrict__ gblock = nullptr) {
   constexpr int HALF = InnerCfg5<W>::HALF, LD = InnerCfg5<W>::LD;
   constexpr int BW = W / 2, NSTEP = W - 1;
   InnerSmem5<W> &S = *reinterpret_cast<InnerSmem5<W> *>(smem);
@@ -266,8 +267,11 @@ __device__ __noinline__ long long inner5_task(unsigned char *smem, const double 
     S.V[i] = (row == col) ? 1.0 : 0.0;
   }
   for (int i = tid; i < NSTEP * W; i += NTH) S.steps[i] = (int8_t)inner[i];
+  // signature of the pair's columns from their global (1-based) indices;
+  // gblock maps a local block-column to its global index (sharded solves)
   for (int j = tid; j < W; j += NTH) {
-    const int64_t gcol = (j < BW ? (int64_t)p0 * BW + j : (int64_t)q0 * BW + (j - BW)) + 1;
+    const int64_t gp = gblock ? gblock[p0] : p0, gq = gblock ? gblock[q0] : q0;
+    const int64_t gcol = (j < BW ? gp * BW + j : gq * BW + (j - BW)) + 1;
     S.sg[j] = gcol <= n_plus ? 1 : -1;
   }
   if (tid == 0) {

@@ -1,4 +1,3 @@
-#include <atomic>
 // The p-step of the blocked one-sided Jacobi (H)SVD on one B200.
 //
 // Reference: run_block_jacobi_inplace / task (pkg/src/jhsvd/driver.py:125-200)
@@ -19,8 +18,7 @@
 #include "jh_common.cuh"
 #include "jh_kernels.h"
 
-#include <cstdio>
-#include <cstdlib>
+#include <atomic>
 
 namespace jh {
 
@@ -30,12 +28,6 @@ constexpr int kGramChunk = 64;     // rows staged per smem chunk
 constexpr int kGramMaxEnt = (kMaxW * (kMaxW + 1) / 2 + kGramThreads - 1) / kGramThreads;
 constexpr int kUpdRows = 128;      // rows per update CTA
 constexpr int kUpdThreads = 256;
-
-struct Workspace {
-  double *H;      // [ntask][w][w]
-  double *Vacc;   // [ntask][w][w]
-  int64_t *rot;   // [ntask] rotations of the task in this p-step
-};
 
 __device__ __forceinline__ const double *pair_col(const double *base, int64_t ld, int p, int q,
                                                   int bw, int j) {
@@ -273,205 +265,6 @@ __device__ InnerOut cta_inner_jacobi(double *R, double *V, int w, const int32_t 
   return out;
 }
 
-// Low-latency variant used by the fused path: the dot products and rotation
-// parameters of all w/2 pairs of an inner p-step are formed by w/2 lanes of
-// warp 0 at once (lane = pair; each lane runs the reference's three in-order
-// fma chains over the w rows of its two columns), published in shared
-// memory, and applied by all threads (one (pair, row) item per thread and
-// matrix).  R and V live in shared memory with column stride w + 1, which
-// keeps the lanes' column reads nearly conflict free.  Two CTA barriers per
-// inner p-step.
-struct Inner2Shared {
-  double cs[kMaxW / 2], tn[kMaxW / 2];
-  int act[kMaxW / 2];   // 0 skip, 1 rotate, 2 rotate + swap; bit 2 = hyperbolic
-  int fail_status, fail_bad, stop;
-  int sweep_rot, sweep_proper;
-};
-
-__device__ InnerOut cta_inner_jacobi2(double *R, double *V, int w, int ld,
-                                      const int32_t *__restrict__ steps, const int8_t *sg,
-                                      double tol_c, int max_sweeps, Inner2Shared *sh) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int half = w / 2;
-  InnerOut out{0, 0, 0, 0, -1};
-  for (int sw = 0; sw < max_sweeps; sw++) {
-    int a_r = 0, b_r = 0;  // per lane of warp 0
-    for (int si = 0; si < w - 1; si++) {
-      const int32_t *st = steps + (size_t)si * half * 2;
-      if (warp == 0) {
-        int act = 0, fail = 0, bad = 0;
-        double cs = 1.0, tn = 0.0;
-        if (lane < half) {
-          const int p = st[2 * lane], q = st[2 * lane + 1];
-          const double *cp = R + p * ld, *cq = R + q * ld;
-          double hpp = 0.0, hqq = 0.0, hpq = 0.0;
-#pragma unroll 8
-          for (int i = 0; i < w; i++) {
-            const double gp = cp[i], gq = cq[i];
-            hpp = fma(gp, gp, hpp);
-            hqq = fma(gq, gq, hqq);
-            hpq = fma(gp, gq, hpq);
-          }
-          if (hpp == 0.0) {
-            fail = kZeroColumn;
-            bad = p + 1;
-          } else if (hqq == 0.0) {
-            fail = kZeroColumn;
-            bad = q + 1;
-          } else if (!(fabs(hpq) < tol_c * sqrt(hpp) * sqrt(hqq))) {
-            const bool hyp = sg[p] > 0 && sg[q] < 0;
-            if (!rotation_core(hpp, hqq, hpq, hyp ? -1.0 : 1.0, cs, tn)) {
-              fail = kHypDomain;
-              bad = p + 1;
-            } else {
-              a_r++;
-              if (cs != 1.0) b_r++;
-              act = 1;
-              if (hyp) {
-                act |= 4;
-              } else {
-                const double h1 = fma(-tn, hpq, hpp);
-                const double h2 = fma(tn, hpq, hqq);
-                if ((sg[p] > 0 && h1 < h2) || (sg[p] < 0 && h1 > h2)) act = 2;
-              }
-            }
-          }
-          sh->act[lane] = act;
-          sh->cs[lane] = cs;
-          sh->tn[lane] = tn;
-        }
-        const unsigned fm = __ballot_sync(0xffffffffu, fail != 0);
-        if (lane == 0) sh->stop = 0;
-        if (fm) {
-          const int first = __ffs(fm) - 1;  // first failing pair in reference order
-          const int fs = __shfl_sync(0xffffffffu, fail, first);
-          const int fb = __shfl_sync(0xffffffffu, bad, first);
-          if (lane == 0) {
-            sh->fail_status = fs;
-            sh->fail_bad = fb;
-            sh->stop = 1;
-          }
-        }
-      }
-      __syncthreads();
-      if (sh->stop) {
-        out.status = sh->fail_status;
-        out.bad = sh->fail_bad;
-        out.sweeps = sw;
-        return out;
-      }
-      // apply: item = (pair, row)
-      for (int it = threadIdx.x; it < half * w; it += blockDim.x) {
-        const int pi = it / w, i = it - pi * w;
-        const int act = sh->act[pi];
-        if (!(act & 3)) continue;
-        const int p = st[2 * pi], q = st[2 * pi + 1];
-        const double cs = sh->cs[pi], tn = sh->tn[pi];
-        const double s = (act & 4) ? tn : -tn;
-        double *rp = R + p * ld + i, *rq = R + q * ld + i;
-        double *vp = V + p * ld + i, *vq = V + q * ld + i;
-        const double gp = *rp, gq = *rq, xp = *vp, xq = *vq;
-        double np = fma(s, gq, gp), nq = fma(tn, gp, gq);
-        double mp = fma(s, xq, xp), mq = fma(tn, xp, xq);
-        if (cs != 1.0) {
-          np = np * cs;
-          nq = nq * cs;
-          mp = mp * cs;
-          mq = mq * cs;
-        }
-        if ((act & 3) == 2) {
-          *rp = nq; *rq = np; *vp = mq; *vq = mp;
-        } else {
-          *rp = np; *rq = nq; *vp = mp; *vq = mq;
-        }
-      }
-      __syncthreads();
-    }
-    // sweep end
-    if (warp == 0) {
-      const int ta = __reduce_add_sync(0xffffffffu, a_r);
-      const int tb = __reduce_add_sync(0xffffffffu, b_r);
-      if (lane == 0) {
-        sh->sweep_rot = ta;
-        sh->sweep_proper = tb;
-      }
-    }
-    __syncthreads();
-    const int ta = sh->sweep_rot, tb = sh->sweep_proper;
-    __syncthreads();
-    out.sweeps++;
-    out.rot += ta;
-    out.proper += tb;
-    if (ta == 0) break;
-  }
-  return out;
-}
-
-// K2 (fast): Cholesky + inner Jacobi, one CTA of kInnerThreads per task.
-constexpr int kInnerThreads = 128;
-
-__global__ void __launch_bounds__(kInnerThreads)
-k_factor_inner2(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
-                int64_t *__restrict__ task_rot, const int32_t *__restrict__ pairs, int bw,
-                int64_t n_plus, const int32_t *__restrict__ inner, int inner_limit,
-                double tol_c, unsigned long long *counters, int pstep) {
-  const int w = 2 * bw, ld = w + 1;
-  const int task = blockIdx.x;
-  const int p = pairs[2 * task], q = pairs[2 * task + 1];
-  extern __shared__ double sm[];
-  double *H = sm;            // w x w, ld w (Cholesky), then R with ld w+1 in Rm
-  double *Rm = sm + w * w;   // w x (w+1)
-  double *V = Rm + w * ld;   // w x (w+1)
-  __shared__ int8_t sg[kMaxW];
-  __shared__ Inner2Shared sh;
-  __shared__ int s_status;
-  const double *Hg = Hbuf + (int64_t)task * w * w;
-  for (int i = threadIdx.x; i < w * w; i += blockDim.x) H[i] = Hg[i];
-  for (int i = threadIdx.x; i < w * ld; i += blockDim.x) {
-    const int col = i / ld, row = i - col * ld;
-    V[i] = (row == col) ? 1.0 : 0.0;
-  }
-  for (int j = threadIdx.x; j < w; j += blockDim.x) {
-    const int64_t gcol = (j < bw ? (int64_t)p * bw + j : (int64_t)q * bw + (j - bw)) + 1;
-    sg[j] = gcol <= n_plus ? 1 : -1;
-  }
-  if (threadIdx.x == 0) s_status = 0;
-  __syncthreads();
-  const int info = cta_cholesky(H, w, &s_status);
-  if (info) {
-    if (threadIdx.x == 0) {
-      task_rot[task] = 0;
-      atomicMin(&counters[2], err_key(pstep, task, kCholesky, info));
-    }
-    return;
-  }
-  // R = L^T: R[i][j] = L[j][i] = H[i*w + j] for i <= j, 0 below
-  for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
-    const int j = e / w, i = e - j * w;
-    Rm[j * ld + i] = (i <= j) ? H[i * w + j] : 0.0;
-  }
-  __syncthreads();
-  const InnerOut o = cta_inner_jacobi2(Rm, V, w, ld, inner, sg, tol_c, inner_limit, &sh);
-  if (o.status) {
-    if (threadIdx.x == 0) {
-      task_rot[task] = 0;
-      atomicMin(&counters[2], err_key(pstep, task, o.status, o.bad));
-    }
-    return;
-  }
-  double *Vg = Vbuf + (int64_t)task * w * w;
-  for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
-    const int j = e / w, i = e - j * w;
-    Vg[e] = V[j * ld + i];
-  }
-  if (threadIdx.x == 0) {
-    task_rot[task] = o.rot;
-    atomicAdd(&counters[0], (unsigned long long)o.rot);
-    atomicAdd(&counters[1], (unsigned long long)o.proper);
-    if (o.rot) atomicAdd(&counters[3], 1ull);
-  }
-}
-
 // K2: Cholesky + inner Jacobi for every task of the p-step; one CTA of
 // 32 * max(1, w/2) threads per task.  Dynamic smem: H/R and V (2 w^2 doubles).
 //   counters[0] += rotations, counters[1] += proper rotations,
@@ -480,7 +273,7 @@ __global__ void k_factor_inner(const double *__restrict__ Hbuf, double *__restri
                                int64_t *__restrict__ task_rot, const int32_t *__restrict__ pairs,
                                int bw, int64_t n_plus, const int32_t *__restrict__ inner,
                                int inner_limit, double tol_c, unsigned long long *counters,
-                               int pstep) {
+                               int pstep, const int32_t *__restrict__ gblock) {
   const int w = 2 * bw;
   const int task = blockIdx.x;
   const int p = pairs[2 * task], q = pairs[2 * task + 1];
@@ -496,7 +289,8 @@ __global__ void k_factor_inner(const double *__restrict__ Hbuf, double *__restri
     V[i] = (i % w == i / w) ? 1.0 : 0.0;
   }
   for (int j = threadIdx.x; j < w; j += blockDim.x) {
-    const int64_t gcol = (j < bw ? (int64_t)p * bw + j : (int64_t)q * bw + (j - bw)) + 1;
+    const int64_t gp = gblock ? gblock[p] : p, gq = gblock ? gblock[q] : q;
+    const int64_t gcol = (j < bw ? gp * bw + j : gq * bw + (j - bw)) + 1;
     sg[j] = gcol <= n_plus ? 1 : -1;
   }
   if (threadIdx.x == 0) s_status = 0;
@@ -631,253 +425,97 @@ __global__ void k_inner_single(double *__restrict__ R, double *__restrict__ V, i
 }
 
 // ---------------------------------------------------------------------------
-// Launch accounting and optional per-kernel-class event timing (bench.py).
+// host side
 
-struct Profiler {
-  bool on = false;
-  int cap = 0, used = 0;
-  cudaEvent_t *ev = nullptr;  // pairs (before, after)
-  int *cls = nullptr;
-};
-static Profiler g_prof;
-// engine 1: overlap the update launch with the inner kernel (jh_set_overlap)
-static bool g_overlap = [] {
-  const char *e = getenv("JHSVD_PDL");
-  return !(e && e[0] == '0');
-}();
-unsigned long long g_launches = 0;
-
-static inline void prof_mark(cudaStream_t st, int cls, bool after) {
-  if (!g_prof.on) return;
-  if (!after) {
-    if (g_prof.used >= g_prof.cap) return;
-    cudaEventRecord(g_prof.ev[2 * g_prof.used], st);
-    g_prof.cls[g_prof.used] = cls;
-  } else {
-    if (g_prof.used >= g_prof.cap) return;
-    cudaEventRecord(g_prof.ev[2 * g_prof.used + 1], st);
-    g_prof.used++;
-  }
+// Workspace of a sweep over a pivot table of `steps` p-steps at order n:
+//   H | V' ring (4 p-steps) | rotation-count ring (4) | per-task done flags
+//   + ready list (engine 1) | second H | per-task G slab counters |
+//   block-column -> task tables (engine 1, Grams in the update launch)
+// The per-task V' and counts of the last four p-steps stay until the paired
+// V pass of engine 1 has read them.
+static int64_t ws_bytes_for(int64_t n, int w, int64_t steps) {
+  const int64_t ntask = n / w, b = 2 * ntask, ww = (int64_t)w * w;
+  if (steps <= 0) steps = b > 1 ? b - 1 : 1;
+  return ntask * ww * 8 * 5 + ntask * 8 * 4 + (2 * ntask + 1) * 8 + ntask * ww * 8 + ntask * 8 +
+         steps * b * 4 + 1024;
 }
 
-}  // namespace jh
-
-using namespace jh;
-
-extern "C" {
-
-// Number of kernels this library has launched (all entry points).
-unsigned long long jh_launch_count(void) { return g_launches; }
-
-// Start timing every p-step kernel launch (up to max_launches launches).
-int jh_profile_begin(int max_launches) {
-  if (g_prof.cap < max_launches) {
-    for (int i = 0; i < 2 * g_prof.cap; i++) cudaEventDestroy(g_prof.ev[i]);
-    delete[] g_prof.ev;
-    delete[] g_prof.cls;
-    g_prof.ev = new cudaEvent_t[2 * (size_t)max_launches];
-    g_prof.cls = new int[max_launches];
-    for (int i = 0; i < 2 * max_launches; i++) cudaEventCreate(&g_prof.ev[i]);
-    g_prof.cap = max_launches;
-  }
-  g_prof.used = 0;
-  g_prof.on = true;
-  return 0;
+static int finish(cudaStream_t) {
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : -(int)e;
 }
 
-// Stop timing; synchronizes on the recorded events and returns per kernel
-// class (0 gram, 1 factor+inner, 2 update, 3 cycle-engine sweep kernel) the
-// summed milliseconds and the number of timed launches (arrays of 4).
-int jh_profile_end(double *ms, int64_t *count) {
-  g_prof.on = false;
-  for (int k = 0; k < 4; k++) {
-    ms[k] = 0.0;
-    count[k] = 0;
-  }
-  for (int i = 0; i < g_prof.used; i++) {
-    float t = 0.f;
-    cudaEventSynchronize(g_prof.ev[2 * i + 1]);
-    cudaEventElapsedTime(&t, g_prof.ev[2 * i], g_prof.ev[2 * i + 1]);
-    ms[g_prof.cls[i]] += t;
-    count[g_prof.cls[i]]++;
-  }
-  return 0;
-}
-
-// Workspace layout shared by the sweep paths: the per-task Gram matrices of
-// one p-step, a ring of four p-steps of per-task V' and rotation counts
-// (engine 1 keeps a p-step's V' until the paired V pass has read it), then
-// the cycle engine's own area (engine 2 only).
-static int64_t ws_base_bytes(int64_t n, int w) {
-  const int64_t ntask = n / w;  // b/2 with b = n / (w/2)
-  // H | V' ring (4) | rotation-count ring (4) | per-task done flags + ready
-  // list (engine 1)
-  // | second H, Gram chain states, per-cycle slab flags (engine 1, fused Gram)
-  // | per-task G slab counters, block-column -> task tables (engine 1, Grams
-  // in the update launch)
-  const int64_t ncyc = ntask / 2 > 0 ? ntask / 2 : 1;
-  const int64_t b = 2 * ntask;
-  return ntask * (int64_t)w * w * 8 * 5 + ntask * 8 * 4 + (2 * ntask + 1) * 8 +
-         ntask * (int64_t)w * w * 8 +
-         ncyc * 2 * 640 * 8 + ncyc * 8 + ntask * 8 + (b > 1 ? b - 1 : 1) * b * 4 + 1024;
-}
-
-// Bytes of device workspace jh_block_sweep (engines 0 and 1) needs.
-int64_t jh_sweep_workspace_bytes(int64_t n, int w) { return ws_base_bytes(n, w); }
-
-// Additional bytes the cycle engine (engine 2) needs after that.
-int64_t jh_cycle_workspace_bytes(int64_t n, int w) { return cycle_workspace_bytes(n, w); }
-
-// Number of int32 entries of the cycle plan of a pivot table of order b
-// (0: order not supported by the cycle engine).
-int64_t jh_cycle_plan_ints(int b) { return cycle_plan_ints(b); }
-
-// Cycle plan of a host pivot table (int32[b-1][b/2][2], 0-based): 0 when
-// every pair of consecutive p-steps (with wrap) pairs the block-columns in
-// 4-cycles, so jh_block_sweep2 can pair or fuse them; 1 otherwise.
-int jh_cycle_plan(const int32_t *outer, int b, int32_t *plan) { return cycle_plan(outer, b, plan); }
-
-// One block sweep (or p-steps [first_step, first_step + nsteps) of it) of
-// run_block_jacobi_inplace (driver.py:180-190) on device data.
-//   G: m x n (ld ldg), V: nv x n (ld ldv) or NULL, both updated in place.
-//   outer: int32[b-1][b/2][2] 0-based block indices (device),
-//   inner: int32[w-1][w/2][2] 0-based column indices (device).
-//   counters (device, uint64[3]): += rotations, += proper, min error key.
-// Returns 0, or a negative CUDA error code.
-int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int64_t ldv,
-                   int64_t nv, int w, const int32_t *outer, int first_step, int nsteps,
-                   const int32_t *inner, int64_t n_plus, int inner_limit, double tol_c,
-                   void *workspace, int64_t ws_bytes, unsigned long long *counters,
-                   void *stream) {
-  if (w < 2 || w % 2 || w > kMaxW || n % w) return -1000;
-  if (ws_bytes < jh_sweep_workspace_bytes(n, w)) return -1001;
-  cudaStream_t st = (cudaStream_t)stream;
+// Engine 0: per p-step K1 Gram, K2 factor + inner Jacobi, K3 update of the
+// rotated tasks' G and V columns.  The DMMA / TMA kernels where the width
+// allows, the generic SIMT kernels otherwise (or when opt_simple()).
+static int sweep_basic(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int64_t ldv,
+                       int64_t nv, int w, const int32_t *outer, const int32_t *gblock,
+                       int first_step, int nsteps, const int32_t *inner, int64_t n_plus,
+                       int inner_limit, double tol_c, void *workspace,
+                       unsigned long long *counters, cudaStream_t st) {
   const int bw = w / 2;
   const int ntask = (int)(n / w);
-  char *ws = (char *)workspace;
-  double *Hbuf = (double *)ws;
-  double *Vbuf = Hbuf + (int64_t)ntask * w * w;                  // ring slot 0
+  double *Hbuf = (double *)workspace;
+  double *Vbuf = Hbuf + (int64_t)ntask * w * w;                    // ring slot 0
   int64_t *trot = (int64_t *)(Hbuf + (int64_t)ntask * w * w * 5);  // ring slot 0
   const int thr_inner = 32 * (bw > 1 ? bw : 1);
   const int nbg = (int)cdiv(m, kUpdRows);
   const int nbv = V ? (int)cdiv(nv, kUpdRows) : 0;
   const size_t smem_gram = sizeof(double) * kGramChunk * w;
   const size_t smem_inner = sizeof(double) * 2 * (size_t)w * w;
-  const size_t smem_inner2 = sizeof(double) * ((size_t)w * w + 2 * (size_t)w * (w + 1));
   const size_t smem_upd = sizeof(double) * ((size_t)w * w + (size_t)w * kUpdRows);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(double) * (kMaxW * kMaxW + kMaxW * kUpdRows)));
-    cudaFuncSetAttribute(k_factor_inner, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(double) * 2 * kMaxW * kMaxW));
-    cudaFuncSetAttribute(k_factor_inner2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(double) * (kMaxW * kMaxW + 2 * kMaxW * (kMaxW + 1))));
-    attr_set = true;
-  }
-  // fast paths (DMMA tiles) unless JHSVD_FORCE_SIMPLE is set (parity tests)
-  static const bool force_simple = getenv("JHSVD_FORCE_SIMPLE") != nullptr;
-  const bool use_tma_gram = !force_simple && gram_tma_ok(w, m, ldg);
-  const bool use_dmma_update = !force_simple && update_dmma_ok(w);
-  // inner-Jacobi kernel variant: 5 (default; fastest at n = 16384 in
-  // tools/bench_inner.py), 4 (register-resident R), 3 (batched applies)
-  static const int inner_variant = [] {
-    const char *e = getenv("JHSVD_INNER");
-    return e ? atoi(e) : 5;
-  }();
-  const bool use_inner4 = !force_simple && inner4_ok(w) && inner_variant == 4;
-  if (!force_simple && inner_variant == 5 && inner5_ok(w)) {
-    for (int s = first_step; s < first_step + nsteps; s++) {
-      const int32_t *pairs = outer + (int64_t)s * ntask * 2;
-      prof_mark(st, 0, false);
-      if (use_tma_gram)
-        launch_gram_tma(G, ldg, m, pairs, ntask, w, Hbuf, st);
-      else
-        k_gram<<<ntask, kGramThreads, smem_gram, st>>>(G, ldg, m, pairs, bw, Hbuf);
-      prof_mark(st, 0, true);
-      prof_mark(st, 1, false);
-      launch_inner5(Hbuf, Vbuf, trot, pairs, ntask, w, n_plus, inner, inner_limit, tol_c, counters,
-                    s, st);
-      prof_mark(st, 1, true);
-      prof_mark(st, 2, false);
-      if (use_dmma_update)
-        launch_update_dmma(G, ldg, m, V, ldv, nv, pairs, ntask, w, Vbuf, trot, st);
-      else
-        k_update<<<dim3(ntask, nbg + nbv), kUpdThreads, smem_upd, st>>>(
-            G, ldg, m, V, ldv, nv, pairs, bw, Vbuf, trot, nbg);
-      prof_mark(st, 2, true);
-      g_launches += 3;
-    }
-    cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? 0 : -(int)e;
-  }
+  ensure_smem((const void *)k_factor_inner, (int)smem_inner);
+  ensure_smem((const void *)k_update, (int)smem_upd);
+  const bool simple = opt_simple();
+  const bool tma_gram = !simple && gram_tma_ok(w, m, ldg);
+  const bool fast_inner = !simple && inner5_ok(w);
+  const bool dmma_update = !simple && update_dmma_ok(w);
   for (int s = first_step; s < first_step + nsteps; s++) {
     const int32_t *pairs = outer + (int64_t)s * ntask * 2;
     prof_mark(st, 0, false);
-    if (use_tma_gram)
+    if (tma_gram)
       launch_gram_tma(G, ldg, m, pairs, ntask, w, Hbuf, st);
     else
       k_gram<<<ntask, kGramThreads, smem_gram, st>>>(G, ldg, m, pairs, bw, Hbuf);
     prof_mark(st, 0, true);
     prof_mark(st, 1, false);
-    if (force_simple)
-      k_factor_inner<<<ntask, thr_inner, smem_inner, st>>>(Hbuf, Vbuf, trot, pairs, bw, n_plus,
-                                                           inner, inner_limit, tol_c, counters, s);
-    else if (use_inner4)
-      launch_inner4(Hbuf, Vbuf, trot, pairs, ntask, w, n_plus, inner, inner_limit, tol_c,
-                    counters, s, st);
-    else if (inner3_ok(w))
-      launch_inner3(Hbuf, Vbuf, trot, pairs, ntask, w, n_plus, inner, inner_limit, tol_c,
-                    counters, s, st);
+    if (fast_inner)
+      launch_inner5(Hbuf, Vbuf, trot, pairs, ntask, w, n_plus, inner, inner_limit, tol_c,
+                    counters, s, st, false, nullptr, 0, gblock);
     else
-      k_factor_inner2<<<ntask, kInnerThreads, smem_inner2, st>>>(
-          Hbuf, Vbuf, trot, pairs, bw, n_plus, inner, inner_limit, tol_c, counters, s);
+      k_factor_inner<<<ntask, thr_inner, smem_inner, st>>>(Hbuf, Vbuf, trot, pairs, bw, n_plus,
+                                                           inner, inner_limit, tol_c, counters, s,
+                                                           gblock);
     prof_mark(st, 1, true);
-    dim3 grid(ntask, nbg + nbv);
     prof_mark(st, 2, false);
-    if (use_dmma_update)
+    if (dmma_update)
       launch_update_dmma(G, ldg, m, V, ldv, nv, pairs, ntask, w, Vbuf, trot, st);
     else
-      k_update<<<grid, kUpdThreads, smem_upd, st>>>(G, ldg, m, V, ldv, nv, pairs, bw, Vbuf, trot,
-                                                    nbg);
+      k_update<<<dim3(ntask, nbg + nbv), kUpdThreads, smem_upd, st>>>(G, ldg, m, V, ldv, nv,
+                                                                     pairs, bw, Vbuf, trot, nbg);
     prof_mark(st, 2, true);
     g_launches += 3;
   }
-  cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? 0 : -(int)e;
-}
-
-// Engine 1: overlap the update launch with the inner Jacobi's tail (1,
-// default) or keep every kernel apart (0, for per-kernel timing).
-int jh_set_overlap(int on) {
-  g_overlap = on != 0;
-  return 0;
-}
-
-// Diagnostic: record one {item, smid, start ns, end ns} int64 record per
-// cycle-engine work item into buf (device, int64[4 + 4 cap]; buf[0] = count)
-// on subsequent launches; buf = NULL disables.
-int jh_cycle_trace(void *buf, int64_t cap) {
-  cycle_trace(buf, cap);
-  return 0;
+  return finish(st);
 }
 
 // Engine 1 (default for rrow-like tables with V accumulated): the
 // per-p-step Gram and inner Jacobi kernels, then one mixed update launch per
-// p-step: the G update CTAs of p-step s (the per-p-step kernel's) and -- the
-// V update deferred to one pass per pair of p-steps (a, a+1) over the
-// 4-cycles of the pair (jh_vpair.cu) -- half of the pair's V row slabs (the
-// other half in the next launch).  V is read by nothing else during the
-// sweep and every V row still receives the same transformations in the same
-// order, so the results are bitwise those of engine 0; V moves through HBM
-// once per two p-steps, and its DMMA-bound slabs share the SMs with the
-// HBM-bound G slabs.  JHSVD_VPAIR=1 runs the V pass as its own launch after
-// the G update instead.  The per-task V' and rotation counts of the last
-// four p-steps are kept in a ring.
+// p-step: the G update CTAs of p-step s and -- the V update deferred to one
+// pass per pair of p-steps (a, a+1) over the 4-cycles of the pair
+// (jh_vpair.cu) -- half of a pair's V row slabs (the other half in the next
+// launch).  V is read by nothing else during the sweep and every V row still
+// receives the same transformations in the same order, so the results are
+// bitwise those of engine 0; V moves through HBM once per two p-steps, and
+// its DMMA-bound slabs share the SMs with the HBM-bound G slabs.  The update
+// launch is a programmatic dependent launch: its CTAs start while the inner
+// kernel's slow tasks finish, each waiting for its own tasks' release flags.
+// For G of at most 2^26 entries the Grams of p-step s+1 run as trailing CTAs
+// of the update launch of p-step s (profiles/r01/cycle_engine.md).
 static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int64_t ldv,
-                         int64_t nv, int w, const int32_t *outer, const int32_t *plan,
-                         int first_step, int nsteps, const int32_t *inner, int64_t n_plus,
-                         int inner_limit, double tol_c, void *workspace,
+                         int64_t nv, int w, const int32_t *outer, int steps, const int32_t *plan,
+                         const int32_t *gblock, int first_step, int nsteps, const int32_t *inner,
+                         int64_t n_plus, int inner_limit, double tol_c, void *workspace,
                          unsigned long long *counters, cudaStream_t st) {
   const int b = (int)(n / (w / 2));
   const int ntask = (int)(n / w);
@@ -887,50 +525,21 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
   int64_t *rring = (int64_t *)(Vring + 4 * (int64_t)ntask * ww);
   int64_t *done = rring + 4 * (int64_t)ntask;
   double *Hbuf2 = (double *)(done + 2 * ntask + 1);
-  double *gstate = Hbuf2 + (int64_t)ntask * ww;
-  int64_t *sflag = (int64_t *)(gstate + (int64_t)(ntask / 2) * 2 * 640);
-  int64_t *gcnt = sflag + (ntask / 2);
+  int64_t *gcnt = (int64_t *)(Hbuf2 + (int64_t)ntask * ww);
   int32_t *colpos = (int32_t *)(gcnt + ntask);
   auto hb = [&](int i) { return (i % 2) ? Hbuf2 : Hbuf; };
   auto vp = [&](int i) { return Vring + (int64_t)(i % 4) * ntask * ww; };
   auto rt = [&](int i) { return rring + (int64_t)(i % 4) * ntask; };
-  static const bool separate = [] {
-    const char *e = getenv("JHSVD_VPAIR");
-    return e && e[0] == '1';
-  }();
-  // overlap of the inner Jacobi's tail with the update (programmatic
-  // dependent launch + per-task flags); JHSVD_PDL=0 or jh_set_overlap(0)
-  // disables (per-kernel timing needs the kernels apart)
-  const bool pdl = g_overlap;
+  const bool pdl = opt_overlap();
   // release-flag epochs: process-wide and atomic, so that solves issued from
   // several host threads never share one
   static std::atomic<int64_t> epoch_ctr{0};
   int64_t epoch = 0;
-  if (pdl && !separate) cudaMemsetAsync(done, 0xff, sizeof(int64_t) * (2 * ntask + 1), st);
-  // opt-in (JHSVD_GU=1): the update launch of p-step s also forms the
-  // Grams of p-step s+1 (one pass over G per p-step, Gram chains handed
-  // from row slab to row slab); bitwise equal but slower on B200 (the
-  // chain hand-offs serialise the slabs of a cycle: 2.33 vs 2.06 ms per
-  // p-step at n = 16384, profiles/r01/cycle_engine.md)
-  static const bool fuse_gram = [] {
-    const char *e = getenv("JHSVD_GU");
-    return e && e[0] == '1';
-  }();
-  const bool gu = fuse_gram && !separate && w == 32;
-  if (gu) cudaMemsetAsync(sflag, 0xff, sizeof(int64_t) * (ntask / 2), st);
-  // Grams of p-step s+1 as trailing CTAs of the update launch of p-step s
-  // (each starts when the G slabs of the two tasks that wrote its
-  // block-columns are done), so the Gram pass overlaps the update's tail
-  // JHSVD_GMIX=1 / 0 forces it on / off; by default on for G of at most
-  // 2^26 entries (n = 8192: 0.626 vs 0.649 ms per p-step, config 2: 0.414
-  // vs 0.428 s); slower for larger G (16384^2: 1.86 vs 1.83 ms per p-step),
-  // profiles/r01/cycle_engine.md
-  static const int gmix_env = [] {
-    const char *e = getenv("JHSVD_GMIX");
-    return e ? (e[0] == '1' ? 1 : 0) : -1;
-  }();
-  const bool gmix = (gmix_env == 1 || (gmix_env < 0 && m * n <= (int64_t(1) << 26))) && !gu && !separate &&
-                    w == 32 && nsteps > 1;
+  if (pdl) cudaMemsetAsync(done, 0xff, sizeof(int64_t) * (2 * ntask + 1), st);
+  // Grams of p-step s+1 in the update launch of p-step s: on for G of at
+  // most 2^26 entries (n = 8192: 0.626 vs 0.649 ms per p-step), off above
+  // (16384^2: 1.86 vs 1.83 ms per p-step)
+  const bool gmix = m * n <= (int64_t(1) << 26) && w == 32 && nsteps > 1;
   if (gmix) {
     cudaMemsetAsync(gcnt, 0, sizeof(int64_t) * ntask, st);
     launch_colpos(outer + (int64_t)first_step * ntask * 2, nsteps, ntask, b, colpos, st);
@@ -939,13 +548,12 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
   for (int i = 0; i < nsteps; i++) {
     const int s = first_step + i;
     const int32_t *pairs = outer + (int64_t)s * ntask * 2;
-    if ((!gu && !gmix) || i == 0) {
+    if (!gmix || i == 0) {
       prof_mark(st, 0, false);
       launch_gram_tma(G, ldg, m, pairs, ntask, w, hb(i), st);
       prof_mark(st, 0, true);
     }
-    const bool use_pdl = pdl && !separate;
-    if (use_pdl) {
+    if (pdl) {
       epoch = ++epoch_ctr;
       cudaMemsetAsync(done + ntask, 0, sizeof(int64_t), st);  // ready-list count
     }
@@ -953,25 +561,9 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
     // overlapped update together)
     prof_mark(st, 1, false);
     launch_inner5(hb(i), vp(i), rt(i), pairs, ntask, w, n_plus, inner, inner_limit, tol_c,
-                  counters, s, st, false, use_pdl ? done : nullptr, epoch);
-    if (!use_pdl) prof_mark(st, 1, true);
+                  counters, s, st, false, pdl ? done : nullptr, epoch, gblock);
+    if (!pdl) prof_mark(st, 1, true);
     const bool last = (i == nsteps - 1);
-    if (separate) {
-      prof_mark(st, 2, false);
-      launch_update_dmma(G, ldg, m, nullptr, 0, 0, pairs, ntask, w, vp(i), rt(i), st);
-      prof_mark(st, 2, true);
-      g_launches += 3;
-      if (i % 2 == 1 || last) {
-        const bool second = (i % 2 == 1);
-        const int i0 = second ? i - 1 : i;
-        prof_mark(st, 3, false);
-        launch_vpair(V, ldv, nv, outer, plan, b, first_step + i0, second, vp(i0), rt(i0),
-                     second ? vp(i) : nullptr, second ? rt(i) : nullptr, st);
-        prof_mark(st, 3, true);
-        g_launches += 1;
-      }
-      continue;
-    }
     // V work: pair j = (2j, 2j+1) is applied to its even row slabs in the
     // launch of p-step 2j+2 and to its odd ones in that of 2j+3, so the V
     // items of a launch never wait for the inner kernel still running;
@@ -996,63 +588,42 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
       nsrc = 0;
       add(i0, sec, kk0, kst);
       prof_mark(st, 3, false);
-      launch_update_mix(G, ldg, 0, pairs, ntask, vp(i), rt(i), V, ldv, nv, outer, plan, b, nsrc,
-                        sa, second, VpA, rotA, VpB, rotB, k0, kstep, st);
+      launch_update_mix(G, ldg, 0, pairs, ntask, vp(i), rt(i), V, ldv, nv, outer, plan, b, steps,
+                        nsrc, sa, second, VpA, rotA, VpB, rotB, k0, kstep, st);
       prof_mark(st, 3, true);
       g_launches += 1;
     };
-    static const bool late_v = [] {  // JHSVD_VSCHED=0: pair j in launches 2j+1 / 2j+2
-      const char *e = getenv("JHSVD_VSCHED");
-      return !(e && e[0] == '0');
-    }();
-    bool tail_single = false;
-    if (late_v) {
-      if (i % 2 == 0 && i >= 2) add(i - 2, true, 0, 2);
-      if (i % 2 == 1 && i >= 3) add(i - 3, true, 1, 2);
-    } else if (i % 2 == 1) {
-      add(i - 1, true, 0, last ? 1 : 2);  // pair (i-1, i): even slabs now, odd ones next
-    } else {
-      if (i >= 2) add(i - 2, true, 1, 2);  // odd slabs of pair (i-2, i-1)
-      if (last) {
-        if (nsrc == 0)
-          add(i, false, 0, 1);
-        else
-          tail_single = true;
-      }
-    }
-    if (!use_pdl) prof_mark(st, 2, false);
-    const bool gu_now = gu && !last;
-    launch_update_mix(G, ldg, m, pairs, ntask, vp(i), rt(i), V, ldv, nv, outer, plan, b, nsrc,
-                      sa, second, VpA, rotA, VpB, rotB, k0, kstep, st, use_pdl ? done : nullptr,
-                      epoch, s, gu_now ? hb(i + 1) : nullptr, gstate, sflag,
+    if (i % 2 == 0 && i >= 2) add(i - 2, true, 0, 2);
+    if (i % 2 == 1 && i >= 3) add(i - 3, true, 1, 2);
+    if (!pdl) prof_mark(st, 2, false);
+    launch_update_mix(G, ldg, m, pairs, ntask, vp(i), rt(i), V, ldv, nv, outer, plan, b, steps,
+                      nsrc, sa, second, VpA, rotA, VpB, rotB, k0, kstep, st,
+                      pdl ? done : nullptr, epoch, s,
                       gmix && !last ? pairs + ntask * 2 : nullptr, colpos + (int64_t)i * b, gcnt,
                       hb(i + 1));
-    prof_mark(st, use_pdl ? 1 : 2, true);
+    prof_mark(st, pdl ? 1 : 2, true);
     g_launches += 3;
-    if (last && late_v) {
+    if (last) {
       if (i % 2 == 1) {
-        flush(i - 1, true, 0, 1);            // the last pair, all slabs
+        flush(i - 1, true, 0, 1);              // the last pair, all slabs
       } else {
         if (i >= 2) flush(i - 2, true, 1, 2);  // odd slabs of the previous pair
         flush(i, false, 0, 1);                 // the last p-step alone
       }
     }
-    if (tail_single) flush(i, false, 0, 1);
   }
-  cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? 0 : -(int)e;
+  return finish(st);
 }
 
 // QR peel-off shortening (shortening = 1, reference blockkernel.py:223-244):
 // per p-step the R factors of every task (jh_qr.cu), the inner Jacobi on R
 // (no Gram, no Cholesky), and the same post-multiplication.
 static int sweep_qr(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int64_t ldv,
-                    int64_t nv, int w, const int32_t *outer, int first_step, int nsteps,
-                    const int32_t *inner, int64_t n_plus, int inner_limit, double tol_c,
-                    void *workspace, int64_t ws_bytes, unsigned long long *counters,
-                    cudaStream_t st) {
-  if (w < 2 || w % 2 || n % w || !qr_ok(w, m)) return -1000;
-  if (ws_bytes < ws_base_bytes(n, w)) return -1001;
+                    int64_t nv, int w, const int32_t *outer, const int32_t *gblock,
+                    int first_step, int nsteps, const int32_t *inner, int64_t n_plus,
+                    int inner_limit, double tol_c, void *workspace,
+                    unsigned long long *counters, cudaStream_t st) {
+  if (!qr_ok(w, m)) return -1000;
   const int ntask = (int)(n / w);
   const int64_t ww = (int64_t)w * w;
   double *Rbuf = (double *)workspace;
@@ -1065,68 +636,67 @@ static int sweep_qr(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int
     prof_mark(st, 0, true);
     prof_mark(st, 1, false);
     launch_inner5(Rbuf, Vbuf, trot, pairs, ntask, w, n_plus, inner, inner_limit, tol_c, counters,
-                  s, st, true);
+                  s, st, true, nullptr, 0, gblock);
     prof_mark(st, 1, true);
     prof_mark(st, 2, false);
     launch_update_dmma(G, ldg, m, V, ldv, nv, pairs, ntask, w, Vbuf, trot, st);
     prof_mark(st, 2, true);
     g_launches += 3;
   }
-  cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? 0 : -(int)e;
+  return finish(st);
 }
 
-// p-steps [first_step, first_step + nsteps) of a block sweep on a chosen
-// engine: 0 = per-p-step kernels (jh_block_sweep), 1 = engine 0 for G with
-// the V update paired over two p-steps on a side stream, 2 = the cycle
-// engine (one persistent kernel, jh_cycle.cu).  Engines 1 and 2 need V (1
-// only), w = 32, even m / ld, and plan = the device copy of jh_cycle_plan's
-// output for this pivot table; otherwise they fall back to engine 0.  All
-// engines give bitwise the same G, V and counters.
-int jh_block_sweep2(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int64_t ldv,
-                    int64_t nv, int w, const int32_t *outer, const int32_t *plan, int engine,
-                    int shortening, int first_step, int nsteps, const int32_t *inner,
-                    int64_t n_plus, int inner_limit, double tol_c, void *workspace,
-                    int64_t ws_bytes, unsigned long long *counters, void *stream) {
-  static const bool force_simple = getenv("JHSVD_FORCE_SIMPLE") != nullptr;
-  if (shortening == 1)
-    return sweep_qr(G, ldg, m, n, V, ldv, nv, w, outer, first_step, nsteps, inner, n_plus,
-                    inner_limit, tol_c, workspace, ws_bytes, counters, (cudaStream_t)stream);
-  if (shortening != 0) return -1000;
-  const int b = (int)(n / (w > 1 ? w / 2 : 1));
-  const bool fused_ok = plan && !force_simple && w % 2 == 0 && n % w == 0 && nsteps > 0 &&
-                        first_step >= 0 && first_step + nsteps <= b - 1 &&
-                        cycle_ok(w, m, ldg, V ? nv : 0, V ? ldv : 0) && gram_tma_ok(w, m, ldg) &&
-                        inner5_ok(w);
+}  // namespace jh
+
+using namespace jh;
+
+extern "C" {
+
+int64_t jh_sweep_workspace_bytes(int64_t n, int w, int64_t steps) {
+  if (w < 2 || w % 2 || n % w) return -1;
+  return ws_bytes_for(n, w, steps);
+}
+
+int64_t jh_cycle_plan_ints(int b, int steps) { return cycle_plan_ints(b, steps); }
+
+int jh_cycle_plan(const int32_t *outer, int b, int steps, int32_t *plan) {
+  return cycle_plan(outer, b, steps, plan);
+}
+
+int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int64_t ldv,
+                   int64_t nv, int w, const int32_t *outer, int outer_steps, const int32_t *plan,
+                   const int32_t *gblock, int engine, int shortening, int first_step, int nsteps,
+                   const int32_t *inner, int64_t n_plus, int inner_limit, double tol_c,
+                   void *workspace, int64_t ws_bytes, unsigned long long *counters,
+                   void *stream) {
+  if (w < 2 || w % 2 || w > kMaxW || n % w || m < 1 || ldg < m) return -1000;
+  if (V && (nv < 1 || ldv < nv)) return -1000;
+  if (first_step < 0 || nsteps < 0 || first_step + nsteps > outer_steps) return -1000;
+  if (ws_bytes < ws_bytes_for(n, w, outer_steps)) return -1001;
+  if (nsteps == 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
-  if (engine == 1 && fused_ok && V) {
-    if (ws_bytes < ws_base_bytes(n, w)) return -1001;
-    return sweep_vpaired(G, ldg, m, n, V, ldv, nv, w, outer, plan, first_step, nsteps, inner,
-                         n_plus, inner_limit, tol_c, workspace, counters, st);
-  }
-  if (engine == 2 && fused_ok) {
-    const int64_t base = ws_base_bytes(n, w);
-    if (ws_bytes < base + cycle_workspace_bytes(n, w)) return -1001;
-    prof_mark(st, 3, false);
-    launch_cycle(G, ldg, m, V, ldv, nv, outer, plan, b, first_step, nsteps, inner, n_plus,
-                 inner_limit, tol_c, counters, (char *)workspace + base, st);
-    prof_mark(st, 3, true);
-    g_launches += 2;
-    cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? 0 : -(int)e;
-  }
-  return jh_block_sweep(G, ldg, m, n, V, ldv, nv, w, outer, first_step, nsteps, inner, n_plus,
-                        inner_limit, tol_c, workspace, ws_bytes, counters, stream);
+  if (shortening == 1)
+    return sweep_qr(G, ldg, m, n, V, ldv, nv, w, outer, gblock, first_step, nsteps, inner, n_plus,
+                    inner_limit, tol_c, workspace, counters, st);
+  if (shortening != 0) return -1000;
+  const bool vpaired_ok = engine == 1 && plan && V && !opt_simple() && w == 32 && m % 2 == 0 &&
+                          ldg % 2 == 0 && nv % 2 == 0 && ldv % 2 == 0;
+  if (vpaired_ok)
+    return sweep_vpaired(G, ldg, m, n, V, ldv, nv, w, outer, outer_steps, plan, gblock,
+                         first_step, nsteps, inner, n_plus, inner_limit, tol_c, workspace,
+                         counters, st);
+  return sweep_basic(G, ldg, m, n, V, ldv, nv, w, outer, gblock, first_step, nsteps, inner,
+                     n_plus, inner_limit, tol_c, workspace, counters, st);
 }
 
-// cholesky_in_place (blockkernel.py:130-145): factors H (c x c, device,
-// overwritten) and writes R = L^T (zero strict lower) to R; *info (device)
-// = 0 or the 1-based bad pivot.
+// cholesky_in_place (blockkernel.py:130-145) of one small matrix (the
+// kernel-level API; the outer level uses jh_potrf): factors H (c x c,
+// device, overwritten) and writes R = L^T (zero strict lower) to R; *info
+// (device) = 0 or the 1-based bad pivot.
 int jh_cholesky(double *H, int c, double *R, int *info, void *stream) {
   g_launches++;
   k_cholesky_single<<<1, 1024, 0, (cudaStream_t)stream>>>(H, c, R, info);
-  const cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? 0 : -(int)e;
+  return finish((cudaStream_t)stream);
 }
 
 // inner_jacobi (blockkernel.py:346-400) on one c x c factor, c even <= 64.
@@ -1134,17 +704,11 @@ int jh_inner_jacobi(double *R, double *V, int c, const int32_t *steps, const int
                     double tol_c, int max_sweeps, int64_t *out, void *stream) {
   if (c < 2 || c % 2 || c > kMaxW) return -1000;
   const size_t smem = sizeof(double) * 2 * (size_t)c * c;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_inner_single, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(double) * 2 * kMaxW * kMaxW));
-    attr = true;
-  }
+  ensure_smem((const void *)k_inner_single, (int)(sizeof(double) * 2 * kMaxW * kMaxW));
   g_launches++;
   k_inner_single<<<1, 32 * (c / 2), smem, (cudaStream_t)stream>>>(R, V, c, steps, signs, tol_c,
                                                                   max_sweeps, out);
-  const cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? 0 : -(int)e;
+  return finish((cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -26,8 +26,20 @@ constexpr int kQrThreads = 128;
 constexpr int kQrWarps = kQrThreads / 32;
 constexpr int kQrMaxW = 32;
 
-// safe bounds (robustnorm.safe_bounds) for vector lengths 0..kQrMaxW
-__constant__ double c_qr_mu[kQrMaxW + 1], c_qr_nu[kQrMaxW + 1];
+// safe bounds (robustnorm.safe_bounds) for vector lengths 0..kQrMaxW, a
+// kernel parameter (no per-device state)
+struct QrBounds {
+  double mu[kQrMaxW + 1], nu[kQrMaxW + 1];
+};
+
+static const QrBounds &qr_bounds() {
+  static const QrBounds b = [] {
+    QrBounds t{};
+    for (int n = 1; n <= kQrMaxW; n++) jh_safe_bounds(n, &t.mu[n], &t.nu[n]);
+    return t;
+  }();
+  return b;
+}
 
 // sum of squares of one leaf restricted to lo <= |x| <= hi, scaled by 2**j
 // (_tree_sumsq_selected with a single leaf)
@@ -46,7 +58,7 @@ __device__ __forceinline__ double qr_selected(const double *x, int n, double lo,
 // norm2_unscaled (robustnorm.py:303-308) of a vector of n <= 256 entries
 // (one leaf), by one thread: _sum_squares_core (robustnorm.py:242-292) then
 // norm2 (:295-300)
-__device__ double qr_norm2(const double *x, int n) {
+__device__ double qr_norm2(const double *x, int n, const QrBounds &bd) {
   if (n == 0) return 0.0;
   double big = 0.0, small = kNu;
   for (int i = 0; i < n; i++) {
@@ -62,7 +74,7 @@ __device__ double qr_norm2(const double *x, int n) {
   if (isfinite(plain) && small * small >= kMu) {
     common_form(0, plain, jr, vr);
   } else {
-    const double mu_tilde = c_qr_mu[n], nu_hat = c_qr_nu[n];
+    const double mu_tilde = bd.mu[n], nu_hat = bd.nu[n];
     int64_t js[3] = {0, 0, 0};
     double vs[3] = {0.0, 0.0, 0.0};
     int count = 0;
@@ -141,12 +153,12 @@ __device__ __forceinline__ void qr_givens(double a, double b, double &cc, double
 // _householder_qr (blockkernel.py:161-188) of a W x W block (column-major,
 // ld W + 1) by one warp; sc: 4 doubles of per-warp scratch
 template <int W>
-__device__ void qr_householder_warp(double *a, double *sc, int lane) {
+__device__ void qr_householder_warp(double *a, double *sc, int lane, const QrBounds &bd) {
   constexpr int LD = W + 1;
   for (int k = 0; k < W - 1; k++) {
     if (lane == 0) {
       const double alpha = a[k * LD + k];
-      const double xnorm = qr_norm2(a + k * LD + k + 1, W - k - 1);
+      const double xnorm = qr_norm2(a + k * LD + k + 1, W - k - 1, bd);
       double skip = 1.0, tau = 0.0, denom = 1.0, beta = 0.0;
       if (xnorm != 0.0) {
         const double nr = qr_hypot2(alpha, xnorm);
@@ -213,13 +225,15 @@ __device__ void qr_peel_warp(double *r0, double *r1, int lane) {
 template <int W>
 __global__ void __launch_bounds__(kQrThreads)
 k_qr_peeloff(const double *__restrict__ G, int64_t ldg, int64_t m,
-             const int32_t *__restrict__ pairs, double *__restrict__ Rbuf) {
+             const int32_t *__restrict__ pairs, double *__restrict__ Rbuf,
+             const __grid_constant__ QrBounds bd) {
   constexpr int LD = W + 1, BW = W / 2;
   __shared__ double r0[W * LD];
   __shared__ double blk[kQrWarps][W * LD];
   __shared__ double sc[kQrWarps][4];
   const int task = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t p = pairs[2 * task], q = pairs[2 * task + 1];
+  // pairs == nullptr: the single pair (0, 1) of jh_qr_peeloff
+  const int64_t p = pairs ? pairs[2 * task] : 0, q = pairs ? pairs[2 * task + 1] : 1;
   const int64_t nchunk = m / W;
   for (int64_t g0 = 0; g0 < nchunk; g0 += kQrWarps) {
     const int64_t c = g0 + warp;
@@ -231,7 +245,7 @@ k_qr_peeloff(const double *__restrict__ G, int64_t ldg, int64_t m,
         a[j * LD + i] = G[col * ldg + c * W + i];
       }
       __syncwarp();
-      qr_householder_warp<W>(a, sc[warp], lane);
+      qr_householder_warp<W>(a, sc[warp], lane, bd);
     }
     __syncthreads();
     if (warp == 0) {
@@ -263,20 +277,11 @@ bool qr_ok(int w, int64_t m) { return (w == 16 || w == 32) && m % w == 0 && m >=
 template <int W>
 static void launch_qr_t(const double *G, int64_t ldg, int64_t m, const int32_t *pairs, int ntask,
                         double *Rbuf, cudaStream_t st) {
-  k_qr_peeloff<W><<<ntask, kQrThreads, 0, st>>>(G, ldg, m, pairs, Rbuf);
+  k_qr_peeloff<W><<<ntask, kQrThreads, 0, st>>>(G, ldg, m, pairs, Rbuf, qr_bounds());
 }
 
 void launch_qr_peeloff(const double *G, int64_t ldg, int64_t m, const int32_t *pairs, int ntask,
                        int w, double *Rbuf, cudaStream_t st) {
-  static bool bounds = false;
-  if (!bounds) {
-    double mu[kQrMaxW + 1], nu[kQrMaxW + 1];
-    mu[0] = nu[0] = 0.0;
-    for (int n = 1; n <= kQrMaxW; n++) jh_safe_bounds(n, &mu[n], &nu[n]);
-    cudaMemcpyToSymbol(c_qr_mu, mu, sizeof(mu));
-    cudaMemcpyToSymbol(c_qr_nu, nu, sizeof(nu));
-    bounds = true;
-  }
   switch (w) {
 #define JH_QR_CASE(W) \
   case W:             \
@@ -297,18 +302,8 @@ void launch_qr_peeloff(const double *G, int64_t ldg, int64_t m, const int32_t *p
 extern "C" int jh_qr_peeloff(const double *A, int64_t lda, int64_t m, int c, double *R,
                              void *stream) {
   if (c < 2 || c > jh::kQrMaxW || c % 2 || m < c || m % c) return -1000;
-  static int32_t *pair01 = nullptr;
-  if (!pair01) {
-    const int32_t h[2] = {0, 1};
-    cudaMalloc(&pair01, sizeof(h));
-    cudaMemcpy(pair01, h, sizeof(h), cudaMemcpyHostToDevice);
-  }
-  jh::launch_qr_peeloff(A, lda, m, pair01, 1, c, R, (cudaStream_t)stream);
+  jh::launch_qr_peeloff(A, lda, m, nullptr, 1, c, R, (cudaStream_t)stream);
   jh::g_launches++;
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : -(int)e;
 }
-
-namespace jh {
-
-}  // namespace jh

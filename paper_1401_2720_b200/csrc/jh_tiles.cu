@@ -206,18 +206,12 @@ bool gram_tma_ok(int w, int64_t m, int64_t ldg) {
 
 // consumer warps per Gram CTA: 2 (tiles 5 + 5 for w = 32), or 4 when few
 // tasks meet long columns (tall factors: one CTA per task leaves SMs short
-// of DMMA warps while every tile is a chain over all m rows); JHSVD_GRAM_NW
-// overrides
+// of DMMA warps while every tile is a chain over all m rows)
 template <int W, int NW, int RCH, int STG>
 static void launch_gram_nw(const double *G, int64_t ldg, int64_t m, const int32_t *pairs,
                            int ntask, double *Hbuf, cudaStream_t st) {
   const size_t smem = sizeof(double) * (size_t)STG * W * (RCH + 4);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_gram_tma<W, NW, RCH, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    attr = true;
-  }
+  ensure_smem((const void *)k_gram_tma<W, NW, RCH, STG>, (int)smem);
   k_gram_tma<W, NW, RCH, STG><<<ntask, 32 * (NW + 1), smem, st>>>(G, ldg, m, pairs, Hbuf);
 }
 
@@ -241,19 +235,8 @@ static void launch_gram_shape(const double *G, int64_t ldg, int64_t m, const int
 template <int W>
 static void launch_gram_t(const double *G, int64_t ldg, int64_t m, const int32_t *pairs,
                           int ntask, double *Hbuf, cudaStream_t st) {
-  static const int env_nw = [] {
-    const char *e = getenv("JHSVD_GRAM_NW");
-    return e ? atoi(e) : 0;
-  }();
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  int nw = env_nw;
-  if (nw != 2 && nw != 4) nw = (ntask < 3 * sms) ? 4 : 2;
-  if (nw == 4)
+  const int sms = sm_count();
+  if (ntask < 3 * sms)
     launch_gram_shape<W, 4>(G, ldg, m, pairs, ntask, sms, Hbuf, st);
   else
     launch_gram_shape<W, 2>(G, ldg, m, pairs, ntask, sms, Hbuf, st);
@@ -274,12 +257,7 @@ static void launch_update_tma_t(double *G, int64_t ldg, int64_t m, double *V, in
                                 int64_t nv, const int32_t *pairs, int ntask, const double *Vbuf,
                                 const int64_t *trot, cudaStream_t st) {
   const size_t smem = sizeof(double) * (size_t)kE0Stages * W * (kE0Rch + 4);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_update_tma<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    attr = true;
-  }
+  ensure_smem((const void *)k_update_tma<W>, (int)smem);
   const int nsg = (int)cdiv(m, kUpdSlab);
   const int nsv = V ? (int)cdiv(nv, kUpdSlab) : 0;
   dim3 grid(ntask, nsg + nsv);
@@ -290,8 +268,8 @@ static void launch_update_tma_t(double *G, int64_t ldg, int64_t m, double *V, in
 void launch_update_dmma(double *G, int64_t ldg, int64_t m, double *V, int64_t ldv, int64_t nv,
                         const int32_t *pairs, int ntask, int w, const double *Vbuf,
                         const int64_t *trot, cudaStream_t st) {
-  static const char *mode = getenv("JHSVD_UPDATE");  // "ldg" selects the LDG variant
-  const bool tma = !(mode && mode[0] == 'l') && m % 2 == 0 && ldg % 2 == 0 &&
+  // the TMA ring needs 16-byte aligned columns; the LDG variant takes the rest
+  const bool tma = m % 2 == 0 && ldg % 2 == 0 &&
                    (!V || (nv % 2 == 0 && ldv % 2 == 0));
   if (tma) {
     if (w == 16)

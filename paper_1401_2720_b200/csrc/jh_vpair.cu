@@ -5,7 +5,7 @@
 // of V by the transforms of p-steps a and a+1 (reference driver.py:165-172,
 // blockkernel.py:407-428) can run as one pass: for the rrow tables, the pairs
 // of two consecutive p-steps form 4-cycles over four block-columns (the
-// cycle plan, jh_cycle.cu), so the 64 V columns of a cycle go through shared
+// cycle plan, jh_plan.cu), so the 64 V columns of a cycle go through shared
 // memory once, get the two step-a transforms and then the two step-(a+1)
 // transforms, and go back -- V moves through HBM once per two p-steps.
 // Every V row still receives the same transformations in the same order
@@ -246,189 +246,6 @@ __device__ __forceinline__ void vpair_cta(const VpArgs &a, int c, int k, VpSmem 
   }
 }
 
-// ---- G update of p-step s fused with the Gram matrices of p-step s+1 ------------
-//
-// A GU item is one 4-cycle c of the step pair (s, s+1) and one row slab k of
-// G.  Its 64 columns (the two step-s tasks t1, t2) stream through the ring;
-// warps 1 and 2 post-multiply them by V'(t1), V'(t2) in place and store the
-// new G straight from the accumulators, warps 3 and 4 continue the Gram
-// chains of the step-(s+1) tasks u1, u2 over the updated rows.  The Gram of
-// u is one in-order DMMA chain per tile over rows 0..m-1 (the reference's
-// fma chain): slab k picks the chains up where slab k-1 left them (a chain
-// state per cycle in global memory, published with a release flag; the
-// grid is slab-major, so slab k-1 of a cycle is always scheduled first) and
-// the last slab writes H for the inner Jacobi of p-step s+1.  G is read
-// once per p-step instead of twice.
-
-constexpr int kGuSlab = 2048;
-
-struct GuArgs {
-  double *G;
-  int64_t ldg, m;
-  const int32_t *outer, *cyc;
-  int S, T, ncyc;
-  int s;                     // p-step of the update; the Grams are for p-step s+1
-  const double *VpA;         // V' of p-step s
-  const int64_t *rotA;
-  const int64_t *done;       // inner-kernel flags of p-step s (programmatic launch) or null
-  int64_t epoch;
-  double *state;             // [ncyc][2][10][32][2] Gram chain states between slabs
-  int64_t *sflag;            // [ncyc] = sepoch * 1024 + (slabs done)
-  int64_t sepoch;
-  double *Hn;                // H of p-step s+1 ([T][W*W])
-  int nslab;
-};
-
-__device__ __forceinline__ void gu_gram_tiles(const double *buf, int nr, const int (&cb)[4],
-                                              double (&acc)[10][2], int g, int t) {
-  const double *c[4];
-#pragma unroll
-  for (int X = 0; X < 4; X++) c[X] = buf + (cb[X] + g) * kVLd + t;
-  auto step = [&](int kk, bool ok) {
-    double f[4];
-#pragma unroll
-    for (int X = 0; X < 4; X++) f[X] = ok ? c[X][4 * kk] : 0.0;
-    int i = 0;
-#pragma unroll
-    for (int X = 0; X < 4; X++)
-#pragma unroll
-      for (int Y = 0; Y <= X; Y++, i++) dmma(acc[i][0], acc[i][1], f[X], f[Y]);
-  };
-  if (nr == kVRch) {
-#pragma unroll 2
-    for (int kk = 0; kk < kVRch / 4; kk++) step(kk, true);
-  } else {
-    const int nks = (nr + 3) / 4;
-    for (int kk = 0; kk < nks; kk++) step(kk, 4 * kk + t < nr);
-  }
-}
-
-__device__ __forceinline__ void gu_cta(const GuArgs &a, int c, int k, VpSmem &S) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const int32_t *cy = a.cyc + ((int64_t)((a.s + 1) % a.S) * a.ncyc + c) * 8;
-  const int tk[2] = {cy[0], cy[1]}, uk[2] = {cy[2], cy[3]};
-  if (a.done) {
-    wait_flag_cta(a.done + tk[0], a.epoch);
-    wait_flag_cta(a.done + tk[1], a.epoch);
-  }
-  const int32_t *pa = a.outer + ((int64_t)a.s * a.T + tk[0]) * 2;
-  const int32_t *pb = a.outer + ((int64_t)a.s * a.T + tk[1]) * 2;
-  int64_t gcol[4] = {(int64_t)pa[0] * 16, (int64_t)pa[1] * 16, (int64_t)pb[0] * 16,
-                     (int64_t)pb[1] * 16};
-  const bool updA[2] = {a.rotA[tk[0]] > 0, a.rotA[tk[1]] > 0};
-  const int ib[2][2] = {{cy[4], cy[5]}, {cy[6], cy[7]}};
-  const int64_t r0 = (int64_t)k * kGuSlab, r1 = min64(r0 + kGuSlab, a.m);
-  const int nchunk = (int)cdiv(r1 - r0, kVRch);
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kVStages; i++) {
-      mbar_init(&S.full[i], 1);
-      mbar_init(&S.adone[i], 2);
-      mbar_init(&S.empty[i], 2);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (warp == 0) {
-    fence_async_global();  // G written by the previous update launch
-    for (int cc = 0; cc < nchunk; cc++) {
-      const int st = cc % kVStages;
-      if (cc >= kVStages) mbar_wait(&S.empty[st], (uint32_t)(((cc / kVStages) - 1) & 1));
-      const int64_t r = r0 + (int64_t)cc * kVRch;
-      const uint32_t bytes = (uint32_t)min64(kVRch, r1 - r) * 8u;
-      if (lane == 0) mbar_expect_tx(&S.full[st], bytes * kVCols);
-      __syncwarp();
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const int j = lane + 32 * h;
-        bulk_g2s(&S.ring[st][j][0], a.G + (gcol[j >> 4] + (j & 15)) * a.ldg + r, bytes,
-                 &S.full[st]);
-      }
-    }
-    return;
-  }
-  const int role = warp - 1, h = role & 1;
-  if (role < 2) {
-    // post-multiplication of task t_h (p-step s), final values to G and to the slot
-    const bool mine = updA[h];
-    double bf[8][4];
-    if (mine) vp_load_bfrag(bf, a.VpA + (int64_t)tk[h] * kVW * kVW, g, t);
-    for (int cc = 0; cc < nchunk; cc++) {
-      const int st = cc % kVStages;
-      mbar_wait(&S.full[st], (uint32_t)((cc / kVStages) & 1));
-      double *buf = &S.ring[st][0][0];
-      const int64_t r = r0 + (int64_t)cc * kVRch;
-      const int nr = (int)min64(kVRch, r1 - r);
-      if (mine) {
-        vp_transform(buf, 32 * h, 32 * h + 16, bf, 0xFu, 0xFu, a.G, a.ldg, gcol, r, nr, g, t);
-        fence_async_smem_cta();
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.adone[st]);
-    }
-    return;
-  }
-  // Gram chains of task u_h (p-step s+1)
-  double acc[10][2];
-  double *st_h = a.state + (((int64_t)c * 2 + h) * 10) * 64;
-  if (k > 0) {
-    if (lane == 0) {
-      const int64_t want = a.sepoch * 1024 + k;
-      for (;;) {
-        int64_t v;
-        asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(a.sflag + c) : "memory");
-        if (v == want) break;
-        __nanosleep(64);
-      }
-    }
-    __syncwarp();
-#pragma unroll
-    for (int i = 0; i < 10; i++) {
-      acc[i][0] = __ldcg(st_h + i * 64 + 2 * lane);
-      acc[i][1] = __ldcg(st_h + i * 64 + 2 * lane + 1);
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < 10; i++) acc[i][0] = acc[i][1] = 0.0;
-  }
-  const int cb[4] = {16 * ib[h][0], 16 * ib[h][0] + 8, 16 * ib[h][1], 16 * ib[h][1] + 8};
-  for (int cc = 0; cc < nchunk; cc++) {
-    const int st = cc % kVStages;
-    mbar_wait(&S.adone[st], (uint32_t)((cc / kVStages) & 1));
-    const int64_t r = r0 + (int64_t)cc * kVRch;
-    const int nr = (int)min64(kVRch, r1 - r);
-    gu_gram_tiles(&S.ring[st][0][0], nr, cb, acc, g, t);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&S.empty[st]);
-  }
-  if (k < a.nslab - 1) {
-#pragma unroll
-    for (int i = 0; i < 10; i++) {
-      st_h[i * 64 + 2 * lane] = acc[i][0];
-      st_h[i * 64 + 2 * lane + 1] = acc[i][1];
-    }
-  } else {
-    double *H = a.Hn + (int64_t)uk[h] * kVW * kVW;
-    int i = 0;
-#pragma unroll
-    for (int X = 0; X < 4; X++)
-#pragma unroll
-      for (int Y = 0; Y <= X; Y++, i++)
-#pragma unroll
-        for (int j = 0; j < 2; j++) {
-          const int x = 8 * X + g, y = 8 * Y + 2 * t + j;
-          H[y * kVW + x] = acc[i][j];
-          if (X != Y) H[x * kVW + y] = acc[i][j];
-        }
-  }
-  // both Gram warps done: publish slab k
-  asm volatile("bar.sync 2, 64;" ::: "memory");
-  if (role == 2 && lane == 0) {
-    __threadfence();
-    asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(a.sflag + c),
-                 "l"(a.sepoch * 1024 + k + 1) : "memory");
-  }
-}
-
 __global__ void __launch_bounds__(160, 2) k_vpair(VpArgs a) {
   extern __shared__ __align__(128) unsigned char smraw[];
   vpair_cta(a, blockIdx.x, blockIdx.y, *reinterpret_cast<VpSmem *>(smraw));
@@ -543,8 +360,6 @@ struct MixArgs {
   VpArgs vp[2];
   int k0[2], kstep[2], nk[2];
   int nsrc, nV;
-  int use_gu;  // G items are GU items (update of p-step s + Grams of p-step s+1)
-  GuArgs gu;
   // Gram items of the next p-step at the end of the grid (nGr of them)
   int nGr;
   const int32_t *pairs_next;  // pair table row of p-step s+1
@@ -601,10 +416,6 @@ __global__ void __launch_bounds__(160, 2) k_update_mix(MixArgs a) {
   }
   if (v1 == v0) {
     const int i = bid - (int)v0;
-    if (a.use_gu) {
-      gu_cta(a.gu, i % a.gu.ncyc, i / a.gu.ncyc, S.v);
-      return;
-    }
     int task = i % a.ntask, slab = i / a.ntask;
     if (a.done) {
       // tasks in the order the inner kernel finishes them (its ready list):
@@ -656,7 +467,7 @@ void launch_colpos(const int32_t *outer, int nsteps, int T, int b, int32_t *colp
 }
 
 void launch_vpair(double *V, int64_t ldv, int64_t nv, const int32_t *outer, const int32_t *plan,
-                  int b, int sa, bool second, const double *VpA, const int64_t *rotA,
+                  int b, int steps, int sa, bool second, const double *VpA, const int64_t *rotA,
                   const double *VpB, const int64_t *rotB, cudaStream_t st) {
   VpArgs a{};
   a.doneA = a.doneB = nullptr;
@@ -665,7 +476,7 @@ void launch_vpair(double *V, int64_t ldv, int64_t nv, const int32_t *outer, cons
   a.nv = nv;
   a.outer = outer;
   a.cyc = plan;
-  a.S = b - 1;
+  a.S = steps;
   a.T = b / 2;
   a.ncyc = a.T / 2;
   a.sa = sa;
@@ -676,23 +487,18 @@ void launch_vpair(double *V, int64_t ldv, int64_t nv, const int32_t *outer, cons
   a.rotB = rotB ? rotB : rotA;
   a.vslab = kVSlab;
   const size_t smem = sizeof(VpSmem);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_vpair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  ensure_smem((const void *)k_vpair, (int)smem);
   dim3 grid(a.ncyc, (unsigned)cdiv(nv, kVSlab));
   k_vpair<<<grid, 160, smem, st>>>(a);
 }
 
 void launch_update_mix(double *G, int64_t ldg, int64_t m, const int32_t *pairs, int ntask,
                        const double *Vbuf, const int64_t *trot, double *V, int64_t ldv,
-                       int64_t nv, const int32_t *outer, const int32_t *plan, int b, int nsrc,
-                       const int *sa, const bool *second, const double *const *VpA,
+                       int64_t nv, const int32_t *outer, const int32_t *plan, int b, int steps,
+                       int nsrc, const int *sa, const bool *second, const double *const *VpA,
                        const int64_t *const *rotA, const double *const *VpB,
                        const int64_t *const *rotB, const int *k0, const int *kstep,
                        cudaStream_t st, const int64_t *done, int64_t epoch, int cur_step,
-                       double *Hnext, double *gstate, int64_t *sflag,
                        const int32_t *pairs_next, const int32_t *colpos, int64_t *gcnt,
                        double *Hgram) {
   MixArgs a{};
@@ -711,31 +517,6 @@ void launch_update_mix(double *G, int64_t ldg, int64_t m, const int32_t *pairs, 
   const int vslab = kMixVSlab[big];
   a.nslab_g = (int)cdiv(m, a.gslab);
   a.nG = ntask * a.nslab_g;
-  if (Hnext) {
-    // G update fused with the Grams of the next p-step
-    static std::atomic<int64_t> sepoch{0};
-    GuArgs &u = a.gu;
-    a.use_gu = 1;
-    u.G = G;
-    u.ldg = ldg;
-    u.m = m;
-    u.outer = outer;
-    u.cyc = plan;
-    u.S = b - 1;
-    u.T = b / 2;
-    u.ncyc = u.T / 2;
-    u.s = cur_step;
-    u.VpA = Vbuf;
-    u.rotA = trot;
-    u.done = done;
-    u.epoch = epoch;
-    u.state = gstate;
-    u.sflag = sflag;
-    u.sepoch = ++sepoch;
-    u.Hn = Hnext;
-    u.nslab = (int)cdiv(m, kGuSlab);
-    a.nG = u.ncyc * u.nslab;
-  }
   const int nslab_v = (int)cdiv(nv, vslab);
   for (int q = 0; q < nsrc && V; q++) {
     VpArgs &v = a.vp[a.nsrc];
@@ -745,7 +526,7 @@ void launch_update_mix(double *G, int64_t ldg, int64_t m, const int32_t *pairs, 
     v.nv = nv;
     v.outer = outer;
     v.cyc = plan;
-    v.S = b - 1;
+    v.S = steps;
     v.T = b / 2;
     v.ncyc = v.T / 2;
     v.sa = sa[q];
@@ -775,11 +556,7 @@ void launch_update_mix(double *G, int64_t ldg, int64_t m, const int32_t *pairs, 
   }
   if (a.nG + a.nV + a.nGr == 0) return;
   const size_t smem = sizeof(MixSmem);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_update_mix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  ensure_smem((const void *)k_update_mix, (int)smem);
   if (!done) {
     k_update_mix<<<a.nG + a.nV + a.nGr, 160, smem, st>>>(a);
     return;

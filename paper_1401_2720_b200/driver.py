@@ -105,16 +105,15 @@ class SweepEngine:
 
     def __init__(self, m: int, n: int, nv: int, cfg: SolverConfig,
                  outer: PStrategy, inner: PStrategy, n_plus: int,
-                 engine: Optional[int] = None):
-        """``engine`` (all bitwise equal, see jh_block_sweep2): 0 per-p-step
+                 engine: Optional[int] = None, outer_table=None, gblock=None):
+        """``engine`` (bitwise equal, see jh_block_sweep): 0 per-p-step
         kernels, 1 per-p-step Gram / inner kernels with the V update paired
         over two p-steps and mixed into the G update launch (default when V
-        is accumulated and the outer table pairs block-columns in 4-cycles,
-        e.g. rrow; falls back to 0 otherwise), 2 the cycle engine (opt-in).
-        JHSVD_ENGINE overrides.  profiles/r01/cycle_engine.md has the
-        measurements."""
-        import os
-
+        is accumulated and the pivot table pairs block-columns in 4-cycles,
+        e.g. rrow; engine 0 otherwise).  ``outer_table`` (int32[steps][b/2][2],
+        0-based) replaces the strategy's table (sharded solves run local
+        sub-tables); ``gblock`` maps local block-columns to global ones for
+        the J signature."""
         import torch
 
         self.lib = _lib.require_cuda()
@@ -131,65 +130,70 @@ class SweepEngine:
         self.cfg = cfg
         self.outer = outer
         self.n_plus = int(n_plus)
-        self.outer_dev = torch.from_numpy(np.array(as_table(outer))).to(dev)
+        table = np.array(as_table(outer) if outer_table is None else outer_table,
+                         dtype=np.int32, order="C")
+        self.table = table
+        self.outer_dev = torch.from_numpy(table).to(dev)
         self.inner_dev = torch.from_numpy(np.array(as_table(inner))).to(dev)
-        self.nsteps = outer.num_steps
-        if engine is None:
-            env = os.environ.get("JHSVD_ENGINE")
-            engine = int(env) if env else (1 if nv > 0 else 0)
-        self.plan_dev = self._cycle_plan(outer) if engine in (1, 2) else None
+        self.nsteps = int(table.shape[0])
+        self.gblock_dev = (torch.from_numpy(np.ascontiguousarray(gblock, dtype=np.int32)).to(dev)
+                           if gblock is not None else None)
+        if engine is None or nv == 0:
+            engine = 1 if nv > 0 else 0
+        self.plan_dev = self._cycle_plan(table) if engine == 1 else None
         self.engine = engine if self.plan_dev is not None else 0
-        nbytes = int(self.lib.jh_sweep_workspace_bytes(n, w))
-        if self.engine == 2:
-            nbytes += int(self.lib.jh_cycle_workspace_bytes(n, w))
+        nbytes = int(self.lib.jh_sweep_workspace_bytes(n, w, self.nsteps))
         self.ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
         self.counters = torch.empty(4, dtype=torch.int64, device=dev)
         self.tasks_rotated: list[int] = []
         self.tol_c = EPS * math.sqrt(w) * cfg.eps_factor
 
-    def _cycle_plan(self, outer: PStrategy):
-        """Device copy of the cycle-engine plan of the outer table (None when
-        the table lacks the 4-cycle structure or the width is not 32)."""
+    def _cycle_plan(self, table: np.ndarray):
+        """Device copy of the 4-cycle plan of the pivot table (None when the
+        table lacks the structure or the width is not 32)."""
         import torch
 
-        b = outer.n
-        nints = int(self.lib.jh_cycle_plan_ints(b)) if self.w == 32 else 0
+        b = 2 * table.shape[1]
+        nints = int(self.lib.jh_cycle_plan_ints(b, table.shape[0])) if self.w == 32 else 0
         if nints <= 0:
             return None
-        table = np.ascontiguousarray(np.array(as_table(outer), dtype=np.int32))
         plan = np.empty(nints, dtype=np.int32)
-        if self.lib.jh_cycle_plan(table.ctypes.data, b, plan.ctypes.data) != 0:
+        if self.lib.jh_cycle_plan(table.ctypes.data, b, table.shape[0], plan.ctypes.data) != 0:
             return None
         return torch.from_numpy(plan).to(_dev.device())
 
     def sweep(self, G, V, first_step: int = 0, nsteps: Optional[int] = None,
-              n_plus: Optional[int] = None):
-        """Enqueue p-steps [first_step, first_step + nsteps) of one block
-        sweep on G (n, m) / V (n, nv) column-major tensors; returns the
-        device counter tensor (rotations, proper, error key, tasks rotated).
-        ``n_plus`` overrides the signature's +1 count for this sweep."""
-        self.counters.zero_()
-        self.counters[2].fill_(-1)
+              n_plus: Optional[int] = None, counters=None):
+        """Enqueue p-steps [first_step, first_step + nsteps) of the pivot table
+        on G (n, m) / V (n, nv) column-major tensors; returns the device
+        counter tensor (rotations, proper, error key, tasks rotated).
+        ``n_plus`` overrides the signature's +1 count; ``counters`` (int64[4],
+        initialised by the caller) accumulates instead of this engine's own."""
+        if counters is None:
+            counters = self.counters
+            counters.zero_()
+            counters[2].fill_(-1)
         ns = self.nsteps - first_step if nsteps is None else nsteps
-        rc = self.lib.jh_block_sweep2(
+        rc = self.lib.jh_block_sweep(
             G.data_ptr(), self.m, self.m, self.n,
             V.data_ptr() if V is not None else None, self.nv, self.nv,
-            self.w, self.outer_dev.data_ptr(),
-            self.plan_dev.data_ptr() if self.plan_dev is not None else None, self.engine,
-            self.shortening, int(first_step), int(ns),
+            self.w, self.outer_dev.data_ptr(), self.nsteps,
+            self.plan_dev.data_ptr() if self.plan_dev is not None else None,
+            self.gblock_dev.data_ptr() if self.gblock_dev is not None else None,
+            self.engine, self.shortening, int(first_step), int(ns),
             self.inner_dev.data_ptr(), self.n_plus if n_plus is None else int(n_plus),
             self.cfg.inner_sweep_limit, self.tol_c,
-            self.ws.data_ptr(), self.ws.numel(), self.counters.data_ptr(),
+            self.ws.data_ptr(), self.ws.numel(), counters.data_ptr(),
             _lib.stream_handle())
         _lib.check(rc, "jh_block_sweep")
-        return self.counters
+        return counters
 
     def raise_error(self, key: int) -> None:
         key &= (1 << 64) - 1
         pstep, task = key >> 38, (key >> 16) & 0x3FFFFF
         status, index = (key >> 13) & 7, key & 0x1FFF
         bw = self.w // 2
-        p, q = (int(x) for x in self.outer_dev[pstep, task].cpu().tolist())
+        p, q = (int(x) for x in self.table[pstep, task])
         gcol = (p * bw + index) if index <= bw else (q * bw + index - bw)
         if status == 1:
             raise RankDeficiencyError(

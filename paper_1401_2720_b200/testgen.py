@@ -221,3 +221,40 @@ def gen_factor_orth_device(sigma, seed: int, m: int | None = None):
     gt = (w * sig.unsqueeze(0)) @ q.t()
     del q, w
     return gt.contiguous()
+
+
+def gen_factor_butterfly_device(sigma, seed: int, m: int | None = None,
+                                n_plus: int | None = None, passes: int = 2,
+                                tanh_max: float = 0.1):
+    """G = Q [diag(sigma); 0] W^T on the GPU (``jh_gen_butterfly``): Q, W
+    random Givens butterflies, plus J-orthogonal hyperbolic layers when
+    ``n_plus == n/2``.  Returns the column-major device storage, an (n, m)
+    tensor whose row i is column i of G.  Bitwise equal to the host twin
+    ``oracle/gen_butterfly.c`` (see ``workloads.py``)."""
+    import torch
+
+    from . import _lib
+
+    lib = _lib.require_cuda()
+    sig = torch.as_tensor(np.ascontiguousarray(sigma, dtype=np.float64), device="cuda")
+    n = int(sig.numel())
+    m = n if m is None else int(m)
+    n_plus = n if n_plus is None else int(n_plus)
+    nbytes = int(lib.jh_gen_workspace_bytes(m, n, n_plus, passes))
+    if nbytes < 0:
+        raise ValueError("jh_gen_butterfly needs m >= n powers of two and n_plus in {n, n/2}")
+    ws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    gt = torch.empty((n, m), dtype=torch.float64, device="cuda")
+    _lib.check(lib.jh_gen_butterfly(gt.data_ptr(), m, m, n, sig.data_ptr(), n_plus, seed,
+                                    passes, tanh_max, ws.data_ptr(), nbytes,
+                                    _lib.stream_handle()), "gen_butterfly")
+    return gt
+
+
+def workload_input_device(wl):
+    """(device storage (n, m), prescribed sigma in generator order, n_plus)
+    of a ``workloads.Workload``."""
+    sigma, n_plus = wl.sigma_nplus()
+    gt = gen_factor_butterfly_device(sigma, wl.gen_seed, m=wl.m, n_plus=n_plus,
+                                     passes=wl.passes, tanh_max=wl.tanh_max)
+    return gt, sigma, n_plus

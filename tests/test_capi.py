@@ -54,4 +54,5 @@ def test_host_safe_bounds_match_reference(kernels_golden):
 
 def test_workspace_size():
     lib = _lib.load_library()
-    assert lib.jh_sweep_workspace_bytes(16384, 32) >= 512 * 32 * 32 * 8 * 2
+    assert lib.jh_sweep_workspace_bytes(16384, 32, 0) >= 512 * 32 * 32 * 8 * 2
+    assert lib.jh_sweep_workspace_bytes(16384, 30, 0) == -1

@@ -1,6 +1,7 @@
 """The branch-free FP64 division / square root fast paths used in the inner
 Jacobi (csrc/jh_fastmath.cuh) must equal the IEEE operators bit for bit
-whenever they report themselves in range."""
+whenever they report themselves in range (probe kernel in the dev-only
+library, tools/dev)."""
 
 import numpy as np
 import pytest
@@ -12,8 +13,10 @@ def _run(a, b):
     import torch
 
     from paper_1401_2720_b200 import _lib
+    from tools.dev import devlib
 
-    lib = _lib.require_cuda()
+    _lib.require_cuda()
+    lib = devlib.load()
     ta = torch.as_tensor(a, dtype=torch.float64, device="cuda")
     tb = torch.as_tensor(b, dtype=torch.float64, device="cuda")
     cnt = torch.zeros(4, dtype=torch.int64, device="cuda")

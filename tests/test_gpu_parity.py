@@ -180,8 +180,10 @@ def test_dmma_probe_runs():
     import torch
 
     from paper_1401_2720_b200 import _lib
+    from tools.dev import devlib
 
-    lib = _lib.require_cuda()
+    _lib.require_cuda()
+    lib = devlib.load()
     nt = 4096
     g = torch.Generator(device="cuda").manual_seed(0)
     A = torch.randn(nt, 32, dtype=torch.float64, device="cuda", generator=g)
@@ -198,42 +200,31 @@ def test_dmma_probe_runs():
     print(f"DMMA vs in-order fma: {mism} of {Dm.numel()} entries differ")
 
 
-@pytest.mark.parametrize("env", [{"JHSVD_I6": "1"}, {"JHSVD_ENGINE": "0", "JHSVD_I6": "1"},
-                                 {"JHSVD_I7": "1"}, {"JHSVD_ENGINE": "0", "JHSVD_I7": "1"},
-                                 {"JHSVD_GMIX": "0"}, {"JHSVD_GMIX": "1"}])
-def test_kernel_variants_bitwise_in_subprocess(env, solves_golden):
-    """Opt-in kernel variants (read once per process from the environment)
-    give the reference golden bitwise: inner variants 6 and 7, Grams in the
-    update launch on / off."""
-    import json
-    import os
-    import subprocess
-    import sys
-    from pathlib import Path
+@pytest.mark.parametrize("simple,overlap", [(1, 1), (0, 0)])
+def test_kernel_paths_bitwise(simple, overlap, solves_golden):
+    """The generic SIMT kernels (jh_set_simple_kernels) and engine 1 with the
+    kernels kept apart (jh_set_overlap(0)) give the reference golden
+    bitwise."""
+    import hashlib
 
-    root = Path(__file__).resolve().parent.parent
-    code = (
-        "import json, hashlib, numpy as np, sys\n"
-        "sys.path.insert(0, '.')\n"
-        "import paper_1401_2720_b200 as J\n"
-        "meta = json.load(open('tests/golden/solves.json'))\n"
-        "arrs = np.load('tests/golden/solves.npz')\n"
-        "sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()\n"
-        "out = {}\n"
-        "for name, m in meta.items():\n"
-        "    r = J.block_jacobi(arrs[name + '_in'], J.Signature(m['n'], m['n_plus']),\n"
-        "                       J.SolverConfig(**m['cfg']))\n"
-        "    out[name] = [sha(r.sigma), [list(s) for s in r.stats],\n"
-        "                 None if r.v is None else sha(np.asfortranarray(r.v).T)]\n"
-        "print(json.dumps(out))\n")
-    e = dict(os.environ)
-    e.update(env)
-    res = subprocess.run([sys.executable, "-c", code], cwd=root, env=e, capture_output=True,
-                         text=True, timeout=600)
-    assert res.returncode == 0, res.stderr[-2000:]
-    got = json.loads(res.stdout.strip().splitlines()[-1])
-    gold, _ = solves_golden
-    for name, g in gold.items():
-        assert got[name][0] == g["sigma_sha256"], (name, env)
-        assert got[name][1] == g["stats"], (name, env)
-        assert got[name][2] == g["v_sha256"], (name, env)
+    import paper_1401_2720_b200 as J
+    from paper_1401_2720_b200 import _lib
+
+    lib = _lib.require_cuda()
+    gold, arrs = solves_golden
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()  # noqa: E731
+    lib.jh_set_simple_kernels(simple)
+    lib.jh_set_overlap(overlap)
+    try:
+        for name, m in gold.items():
+            cfg = J.SolverConfig(**m["cfg"])
+            if cfg.shortening == "qr" and simple:
+                continue
+            r = J.block_jacobi(arrs[name + "_in"], J.Signature(m["n"], m["n_plus"]), cfg)
+            assert sha(r.sigma) == m["sigma_sha256"], name
+            assert [list(s) for s in r.stats] == m["stats"], name
+            if m["v_sha256"] is not None:
+                assert sha(np.asfortranarray(r.v).T) == m["v_sha256"], name
+    finally:
+        lib.jh_set_simple_kernels(0)
+        lib.jh_set_overlap(1)

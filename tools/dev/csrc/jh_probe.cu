@@ -2,8 +2,8 @@
 // (mma.sync m8n8k4 f64, SASS DMMA) against an in-order fma chain over k.
 // If DMMA rounds after every k term in ascending order, the Gram and update
 // contractions can run on DMMA tiles and stay bitwise equal to the reference
-// (hard part H1).  Used by tests/ and the probe script;
-// not on the solver path.
+// (hard part H1).  Dev-only library (tools/dev):
+// used by tests/ and the probe scripts, never by the solver.
 #include "jh_common.cuh"
 #include "jh_fastmath.cuh"
 
@@ -40,7 +40,6 @@ extern "C" int jh_probe_dmma(const double *A, const double *B, const double *C, 
                              double *Df, int ntests, void *stream) {
   const int threads = 256;
   const int blocks = (ntests * 32 + threads - 1) / threads;
-  jh::g_launches++;
   jh::k_probe_dmma<<<blocks, threads, 0, (cudaStream_t)stream>>>(A, B, C, Dm, Df, ntests);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : -(int)e;

@@ -14,10 +14,12 @@ import torch
 
 sys.path.insert(0, ".")
 from paper_1401_2720_b200 import _lib  # noqa: E402
+from tools.dev import devlib  # noqa: E402
 
 
 def main(out="gpurun_out/dmma_probe.json"):
-    lib = _lib.require_cuda()
+    _lib.require_cuda()
+    lib = devlib.load()
     nt = 8192
     g = torch.Generator(device="cuda").manual_seed(1)
     A = torch.randn(nt, 32, dtype=torch.float64, device="cuda", generator=g)

@@ -6,10 +6,12 @@ import torch
 
 sys.path.insert(0, ".")
 from paper_1401_2720_b200 import _lib  # noqa: E402
+from tools.dev import devlib  # noqa: E402
 
 
 def main():
-    lib = _lib.require_cuda()
+    _lib.require_cuda()
+    lib = devlib.load()
     out = torch.zeros(1, dtype=torch.float64, device="cuda")
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     res = []
@@ -49,7 +51,8 @@ def timed(lib, kind, ctas, threads, iters, out):
 def chains_and_mixed():
     """DMMA rate vs independent chains per warp (1 warp per SMSP, i.e. 4 per
     SM, and 1 per SM), and DMMA + DFMA warps side by side."""
-    lib = _lib.require_cuda()
+    _lib.require_cuda()
+    lib = devlib.load()
     out = torch.zeros(1, dtype=torch.float64, device="cuda")
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     clk = torch.cuda.clock_rate() if hasattr(torch.cuda, "clock_rate") else None
@@ -80,7 +83,8 @@ elif __name__ == "__main__" and "--latency" not in sys.argv:
 
 
 def latency():
-    lib = _lib.require_cuda()
+    _lib.require_cuda()
+    lib = devlib.load()
     out = torch.zeros(9, dtype=torch.float64, device="cuda")
     for _ in range(2):
         _lib.check(lib.jh_probe_latency(out.data_ptr(), _lib.stream_handle()), "lat")
