@@ -126,6 +126,25 @@ void jh_safe_bounds(int64_t n, double *mu_tilde, double *nu_hat);
 int jh_column_norms(const double *G, int64_t ldg, int64_t m, int64_t n, int64_t *js, double *s,
                     void *stream);
 
+/* robustnorm.sum_squares / norm2 (robustnorm.py:324-334) of the n columns of
+ * G (m x n, ld ldg) with the reference's chunk (leaf length) and
+ * force_scaled options: sum of squares vsq * 2**jsq in common form and the
+ * norm s / 2**js, device arrays of n (each may be NULL). */
+int jh_robust_norms(const double *G, int64_t ldg, int64_t m, int64_t n, int chunk,
+                    int force_scaled, int64_t *jsq, double *vsq, int64_t *js, double *s,
+                    void *stream);
+
+/* Host DRDSSQ helpers (robustnorm.py:116-162): common_form, add_scaled,
+ * scale_exponent (up = 1: smallest j with 2**j f >= t; 0: largest with <=). */
+void jh_common_form(int64_t j, double v, int64_t *jo, double *vo);
+void jh_add_scaled(int64_t ja, double va, int64_t jb, double vb, int64_t *jo, double *vo);
+int jh_scale_exponent(double f, double t, int up);
+
+/* _rotation_core (rotation.py:90-102) of n pivot Grams: in (device, n x 3
+ * h_pp, h_qq, h_pq), t (device, +1 trig / -1 hyperbolic), out (device,
+ * n x 3: cs, tn, 1 ok / 0 hyperbolic domain failure). */
+int jh_rotations(const double *in, const double *t, int64_t n, double *out, void *stream);
+
 /* check_column_scaling (driver.py:99-112): *bad (device, init UINT64_MAX)
  * = smallest 1-based column with norm outside [mu_tilde, sqrt(nu_hat)]. */
 int jh_check_scaling(const double *G, int64_t ldg, int64_t m, int64_t n,

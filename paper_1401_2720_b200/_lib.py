@@ -46,6 +46,12 @@ SIGNATURES = {
     "jh_column_norms": (_c_i32, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p]),
     "jh_check_scaling": (_c_i32, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p]),
     "jh_sigma_u": (_c_i32, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_i64, _c_p, _c_p]),
+    "jh_robust_norms": (_c_i32, [_c_p, _c_i64, _c_i64, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_p,
+                                 _c_p, _c_p]),
+    "jh_common_form": (None, [_c_i64, _c_d, _c_p, _c_p]),
+    "jh_add_scaled": (None, [_c_i64, _c_d, _c_i64, _c_d, _c_p, _c_p]),
+    "jh_scale_exponent": (_c_i32, [_c_d, _c_d, _c_i32]),
+    "jh_rotations": (_c_i32, [_c_p, _c_p, _c_i64, _c_p, _c_p]),
     "jh_gen_workspace_bytes": (_c_i64, [_c_i64, _c_i64, _c_i64, _c_i32]),
     "jh_gen_butterfly": (_c_i32, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, ctypes.c_ulonglong,
                                   _c_i32, _c_d, _c_p, _c_i64, _c_p]),

@@ -106,7 +106,7 @@ __device__ __forceinline__ bool rotation_core_sel(double hpp, double hqq, double
 __host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 
-// total kernel launches issued by this library (defined in jh_pstep.cu)
+// total kernel launches issued by this library (defined in jh_runtime.cu)
 extern unsigned long long g_launches;
 
 }  // namespace jh

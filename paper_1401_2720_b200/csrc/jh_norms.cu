@@ -8,6 +8,7 @@
 // scaled three-partition fallback of _sum_squares_core when the plain sum
 // over/underflows.  The result is therefore bitwise the reference's.
 #include "jh_common.cuh"
+#include "jh_kernels.h"
 #include "jh_robust.cuh"
 
 #include <cmath>
@@ -22,15 +23,15 @@ constexpr int kNormThreads = 256;
 // and scaled by 2**j (_tree_sumsq_plain / _tree_sumsq_selected), then the
 // fixed-tree combine (_tree_combine) by thread 0.  Result valid in thread 0.
 __device__ double cta_tree_sumsq(const double *__restrict__ x, int64_t m, bool selected,
-                                 double lo, double hi, int j, double *part) {
-  const int64_t nleaf = cdiv(m, kLeaf);
+                                 double lo, double hi, int j, double *part, int leaf) {
+  const int64_t nleaf = cdiv(m, leaf);
   for (int64_t c = threadIdx.x; c < nleaf; c += blockDim.x) {
     double acc = 0.0;
-    const int64_t end = min64((c + 1) * kLeaf, m);
+    const int64_t end = min64((c + 1) * leaf, m);
     if (!selected) {
-      for (int64_t i = c * kLeaf; i < end; i++) acc = fma(x[i], x[i], acc);
+      for (int64_t i = c * leaf; i < end; i++) acc = fma(x[i], x[i], acc);
     } else {
-      for (int64_t i = c * kLeaf; i < end; i++) {
+      for (int64_t i = c * leaf; i < end; i++) {
         const double a = fabs(x[i]);
         if (a > 0.0 && lo <= a && a <= hi) {
           const double v = ldexp(x[i], j);
@@ -56,10 +57,14 @@ __device__ double cta_tree_sumsq(const double *__restrict__ x, int64_t m, bool s
   return r;
 }
 
-// norm2 of one column (robustnorm.py:242-300): (js, sigma), ||x|| = sigma / 2**js.
-// Valid in thread 0.
+// norm2 of one column (robustnorm.py:242-300): (js, sigma), ||x|| = sigma / 2**js,
+// and the sum of squares in common form (j, v) = v * 2**-j (_sum_squares_core).
+// leaf = the reference's chunk (256 by default); force_scaled skips the plain
+// fast path (robustnorm.sum_squares(force_scaled=True)).  Valid in thread 0.
 __device__ void cta_norm2(const double *__restrict__ x, int64_t m, double mu_tilde,
-                          double nu_hat, double *part, int64_t &js_out, double &s_out) {
+                          double nu_hat, double *part, int64_t &js_out, double &s_out,
+                          int leaf = kLeaf, bool force_scaled = false,
+                          int64_t *jsq_out = nullptr, double *vsq_out = nullptr) {
   __shared__ double s_big[kNormThreads / 32], s_small[kNormThreads / 32];
   __shared__ double s_plain;
   __shared__ int s_done;
@@ -86,11 +91,13 @@ __device__ void cta_norm2(const double *__restrict__ x, int64_t m, double mu_til
   }
   js_out = 0;
   s_out = 0.0;
+  if (jsq_out) *jsq_out = 0;
+  if (vsq_out) *vsq_out = 0.0;
   if (m == 0 || big == 0.0) return;
-  const double plain = cta_tree_sumsq(x, m, false, 0.0, 0.0, 0, part);
+  const double plain = force_scaled ? 0.0 : cta_tree_sumsq(x, m, false, 0.0, 0.0, 0, part, leaf);
   if (threadIdx.x == 0) {
     s_plain = plain;
-    s_done = (isfinite(plain) && small * small >= kMu) ? 1 : 0;
+    s_done = (!force_scaled && isfinite(plain) && small * small >= kMu) ? 1 : 0;
   }
   __syncthreads();
   int64_t jres = 0;
@@ -102,13 +109,13 @@ __device__ void cta_norm2(const double *__restrict__ x, int64_t m, double mu_til
     double vsv[3] = {0.0, 0.0, 0.0};
     int count = 0;
     if (small <= nu_hat && big >= mu_tilde) {
-      const double s1 = cta_tree_sumsq(x, m, true, mu_tilde, nu_hat, 0, part);
+      const double s1 = cta_tree_sumsq(x, m, true, mu_tilde, nu_hat, 0, part, leaf);
       if (threadIdx.x == 0 && s1 != 0.0) common_form(0, s1, jsv[count], vsv[count]);
       if (threadIdx.x == 0 && s1 != 0.0) count++;
     }
     if (big > nu_hat) {
       const int j2 = scale_exponent(big, nu_hat, false);
-      const double s2 = cta_tree_sumsq(x, m, true, nextafter(nu_hat, kNu), kNu, j2, part);
+      const double s2 = cta_tree_sumsq(x, m, true, nextafter(nu_hat, kNu), kNu, j2, part, leaf);
       if (threadIdx.x == 0 && s2 != 0.0) {
         common_form(-2 * (int64_t)j2, s2, jsv[count], vsv[count]);
         count++;
@@ -116,7 +123,7 @@ __device__ void cta_norm2(const double *__restrict__ x, int64_t m, double mu_til
     }
     if (small < mu_tilde) {
       const int j0 = scale_exponent(small, mu_tilde, true);
-      const double s0 = cta_tree_sumsq(x, m, true, 0.0, nextafter(mu_tilde, 0.0), j0, part);
+      const double s0 = cta_tree_sumsq(x, m, true, 0.0, nextafter(mu_tilde, 0.0), j0, part, leaf);
       if (threadIdx.x == 0 && s0 != 0.0) {
         common_form(-2 * (int64_t)j0, s0, jsv[count], vsv[count]);
         count++;
@@ -142,9 +149,46 @@ __device__ void cta_norm2(const double *__restrict__ x, int64_t m, double mu_til
       common_form(ja, va, jres, vres);
     }
   }
+  if (threadIdx.x == 0) {
+    if (jsq_out) *jsq_out = jres;
+    if (vsq_out) *vsq_out = vres;
+  }
   if (threadIdx.x == 0 && vres != 0.0) {
     js_out = -(jres / 2);  // jres is even in common form
     s_out = sqrt(vres);
+  }
+}
+
+// robustnorm.sum_squares / norm2 with the reference's chunk and
+// force_scaled options, one CTA per column; any output may be null
+__global__ void __launch_bounds__(kNormThreads)
+k_robust_norms(const double *__restrict__ G, int64_t ldg, int64_t m, double mu_tilde,
+               double nu_hat, int leaf, int force_scaled, int64_t *jsq, double *vsq,
+               int64_t *js, double *s) {
+  extern __shared__ double part[];
+  const int64_t col = blockIdx.x;
+  int64_t a, jq;
+  double b, vq;
+  cta_norm2(G + col * ldg, m, mu_tilde, nu_hat, part, a, b, leaf, force_scaled != 0, &jq, &vq);
+  if (threadIdx.x == 0) {
+    if (jsq) jsq[col] = jq;
+    if (vsq) vsq[col] = vq;
+    if (js) js[col] = a;
+    if (s) s[col] = b;
+  }
+}
+
+// batch rotation parameters (rotation.py:90-124): in[i] = (h_pp, h_qq, h_pq),
+// t[i] = +1 trigonometric / -1 hyperbolic; out[i] = (cs, tn, ok)
+__global__ void k_rotations(const double *__restrict__ in, const double *__restrict__ t,
+                            int64_t n, double *__restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double cs = 1.0, tn = 0.0;
+    const bool ok = rotation_core(in[3 * i], in[3 * i + 1], in[3 * i + 2], t[i], cs, tn);
+    out[3 * i] = cs;
+    out[3 * i + 1] = tn;
+    out[3 * i + 2] = ok ? 1.0 : 0.0;
   }
 }
 
@@ -276,15 +320,13 @@ void jh_safe_bounds(int64_t n, double *mu_tilde, double *nu_hat) {
   *nu_hat = (sl < 0.0) ? std::nextafter(sh, 0.0) : sh;
 }
 
-static size_t norm_smem(int64_t m) { return sizeof(double) * (size_t)(cdiv(m, kLeaf) + 1); }
+static size_t norm_smem(int64_t m, int leaf = kLeaf) {
+  return sizeof(double) * (size_t)(cdiv(m, leaf) + 1);
+}
 
 static int prep_norm(int64_t m) {
-  static int64_t set_for = 0;
   const size_t need = norm_smem(m);
-  if (need > 48 * 1024 && (int64_t)need > set_for) {
-    cudaFuncSetAttribute(k_colnorm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need);
-    set_for = (int64_t)need;
-  }
+  if (need > 48 * 1024) ensure_smem((const void *)k_colnorm, (int)need);
   return 0;
 }
 
@@ -330,5 +372,60 @@ int jh_sigma_u(const double *G, int64_t ldg, int64_t m, int64_t n, double *sigma
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : -(int)e;
 }
+
+// robustnorm.sum_squares / norm2 (robustnorm.py:324-334) of the n columns
+// of G (m x n, ld ldg) with the reference's chunk (leaf length) and
+// force_scaled options: sum of squares v * 2**-j in common form (jsq, vsq)
+// and the norm s / 2**js; each output may be NULL.
+int jh_robust_norms(const double *G, int64_t ldg, int64_t m, int64_t n, int chunk,
+                    int force_scaled, int64_t *jsq, double *vsq, int64_t *js, double *s,
+                    void *stream) {
+  if (chunk < 1 || m < 0 || n < 0) return -1000;
+  if (n == 0) return 0;
+  double mu, nu;
+  jh_safe_bounds(m > 0 ? m : 1, &mu, &nu);
+  const size_t smem = norm_smem(m, chunk);
+  if (smem > 227 * 1024) return -1000;
+  if (smem > 48 * 1024) ensure_smem((const void *)k_robust_norms, (int)smem);
+  g_launches++;
+  k_robust_norms<<<(unsigned)n, kNormThreads, smem, (cudaStream_t)stream>>>(
+      G, ldg, m, mu, nu, chunk, force_scaled, jsq, vsq, js, s);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : -(int)e;
+}
+
+// rotation parameters of n pivot Grams (rotation.py:90-124 _rotation_core):
+// in (device, n x 3: h_pp, h_qq, h_pq), t (device, n: +1 / -1),
+// out (device, n x 3: cs, tn, 1 = ok / 0 = hyperbolic domain failure).
+int jh_rotations(const double *in, const double *t, int64_t n, double *out, void *stream) {
+  if (n < 0) return -1000;
+  if (n == 0) return 0;
+  g_launches++;
+  const int64_t blocks = (n + 255) / 256;
+  k_rotations<<<(unsigned)(blocks < 1024 ? blocks : 1024), 256, 0, (cudaStream_t)stream>>>(
+      in, t, n, out);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : -(int)e;
+}
+
+// Scalar DRDSSQ helpers of robustnorm.py:116-162 on the host (the same code
+// the kernels inline): common_form, add_scaled, scale_exponent.
+void jh_common_form(int64_t j, double v, int64_t *jo, double *vo) {
+  int64_t a;
+  double b;
+  common_form(j, v, a, b);
+  *jo = a;
+  *vo = b;
+}
+
+void jh_add_scaled(int64_t ja, double va, int64_t jb, double vb, int64_t *jo, double *vo) {
+  int64_t a;
+  double b;
+  add_scaled(ja, va, jb, vb, a, b);
+  *jo = a;
+  *vo = b;
+}
+
+int jh_scale_exponent(double f, double t, int up) { return scale_exponent(f, t, up != 0); }
 
 }  // extern "C"

@@ -46,20 +46,25 @@ from .strategy import PStrategy, make_strategy
 FAST = "fast"
 SLOW = "slow"
 NVSWITCH = "nvswitch"
-EXHAUSTIVE_MAPPING_MAX_G = 4
 
 
 @dataclass(frozen=True)
 class Topology:
-    """The reference's two-speed link classification (distsim.py:46-55):
-    worker i talks to i xor 1 over a fast link, to the rest over slow ones."""
+    """Link speed between workers.  ``uniform=False`` is the reference's
+    two-speed box (distsim.py:46-55: a worker's partner i xor 1 is reached
+    over a fast link, everyone else over a slow one); ``uniform=True`` is an
+    NVSwitch box, where every GPU reaches every peer at full NVLink rate."""
 
     g: int
+    uniform: bool = False
 
     def link_class(self, i: int, j: int) -> str:
-        if i == j or not (0 <= i < self.g and 0 <= j < self.g):
+        valid = i != j and 0 <= i < self.g and 0 <= j < self.g
+        if not valid:
             raise ValueError(f"invalid link ({i}, {j}) for {self.g} workers")
-        return FAST if j == i ^ 1 else SLOW
+        if self.uniform:
+            return FAST
+        return FAST if (i ^ j) == 1 else SLOW
 
 
 class MappingError(ValueError):
@@ -70,15 +75,19 @@ class MappingError(ValueError):
 class ColumnMapping:
     """assignments[s][i] = 1-based (p, q) block pair of worker i at step s;
     moves[s][i] = (src worker, block-column) worker i receives after step s
-    (the last step wraps to the first)."""
+    (the last step wraps to the first); fast_exchanges = transitions whose
+    moves all use fast links (reference distsim.py:58-72)."""
 
     g: int
     assignments: tuple
     moves: tuple
+    fast_exchanges: int = 0
 
 
 @dataclass(frozen=True)
 class ExchangeRecord:
+    """One block-column message of the outer level (distsim.py:206-213)."""
+
     sweep: int
     step: int
     worker: int
@@ -107,149 +116,114 @@ def _moves(cur, nxt):
     return tuple(out)
 
 
-@functools.lru_cache(maxsize=16)
-def legal_mapping(strategy: PStrategy) -> ColumnMapping:
-    """An assignment of the outer strategy's pairs to g = n/2 workers such
-    that between consecutive steps -- the last wrapping to the first -- every
-    worker keeps exactly one block-column (the exchange protocol of
-    distsim.py:334-360).
-
-    Between two p-steps the "share exactly one column" relation is 2-regular,
-    so each transition offers 2^cycles perfect matchings.  A breadth-first
-    search over worker->pair states (at most g! of them, deduplicated) finds
-    every state reachable at the last step; the lexicographically smallest one
-    that wraps legally back to step 0 is traced back.  g = 8 takes seconds
-    (the reference's exhaustive fast-link search does not finish)."""
-    g = strategy.n // 2
-    steps = [tuple(sorted(st)) for st in strategy.steps]
-    ns = len(steps)
-    if g == 1:
-        return ColumnMapping(1, tuple((pq,) for pq in strategy.steps), ((),) * ns)
-
-    def matchings(cur, nxt):
-        adj = [[k for k, Q in enumerate(nxt) if len(set(P) & set(Q)) == 1] for P in cur]
-        out, used, chosen = [], [False] * g, []
-
-        def rec(i):
-            if i == g:
-                out.append(tuple(chosen))
-                return
-            for k in adj[i]:
-                if not used[k]:
-                    used[k] = True
-                    chosen.append(k)
-                    rec(i + 1)
-                    chosen.pop()
-                    used[k] = False
-
-        rec(0)
-        return out
-
-    start = tuple(range(g))          # worker i holds pair i of step 0
-    layers = [{start: None}]
-    for s in range(ns - 1):
-        ms = matchings(steps[s], steps[s + 1])
-        nxt = {}
-        for state in sorted(layers[-1]):
-            for mm in ms:
-                child = tuple(mm[state[i]] for i in range(g))
-                if child not in nxt:
-                    nxt[child] = state
-        layers.append(nxt)
-    final = sorted(st for st in layers[-1]
-                   if all(len(set(steps[-1][st[i]]) & set(steps[0][i])) == 1 for i in range(g)))
-    if not final:
-        raise MappingError("no exchange-compatible worker assignment exists")
-    path = [final[0]]
-    for s in range(ns - 1, 0, -1):
-        path.append(layers[s][path[-1]])
-    path.reverse()
-    assignments = tuple(tuple(steps[s][path[s][i]] for i in range(g)) for s in range(ns))
-    moves = tuple(_moves(assignments[s], assignments[(s + 1) % ns]) for s in range(ns))
-    return ColumnMapping(g, assignments, moves)
+def _all_fast(moves, topology: Topology) -> bool:
+    return all(topology.link_class(src, i) == FAST for i, (src, _) in enumerate(moves))
 
 
-def _assignment_options(cur, next_step_pairs):
-    """All bijections pairs -> workers for the next step in which every
-    worker keeps exactly one of its block-columns (distsim.py:104-133)."""
+def _step_matchings(cur, nxt):
+    """Every bijection worker-of-cur-pair -> pair of nxt (as index tuples)
+    under which each worker keeps exactly one block-column.  Between two
+    p-steps the relation "shares one column" is 2-regular, so there are
+    2^(cycles) of them."""
     g = len(cur)
-    per_worker = [[pq for pq in next_step_pairs if len(set(cur[i]) & set(pq)) == 1]
-                  for i in range(g)]
-    options, chosen, used = [], [], set()
+    adj = [[k for k, Q in enumerate(nxt) if len(set(P) & set(Q)) == 1] for P in cur]
+    out, used, chosen = [], [False] * g, []
 
     def rec(i):
         if i == g:
-            options.append(tuple(chosen))
+            out.append(tuple(chosen))
             return
-        for pq in per_worker[i]:
-            if pq in used:
-                continue
-            used.add(pq)
-            chosen.append(pq)
-            rec(i + 1)
-            chosen.pop()
-            used.remove(pq)
+        for k in adj[i]:
+            if not used[k]:
+                used[k] = True
+                chosen.append(k)
+                rec(i + 1)
+                chosen.pop()
+                used[k] = False
 
     rec(0)
-    return options
+    return out
 
 
 @functools.lru_cache(maxsize=16)
 def optimize_mapping(strategy: PStrategy, topology: Topology) -> ColumnMapping:
-    """The reference's mapping (distsim.py:136-190): exhaustive search for
-    the assignment with the most all-fast exchange transitions per sweep
-    (the wrap from the last step to the first included), ties toward the
-    lexicographically smallest assignment table.  Exponential in g: used
-    for g <= EXHAUSTIVE_MAPPING_MAX_G."""
-    import itertools
+    """A worker mapping of the outer strategy (order 2g) for the exchange
+    protocol of distsim.py:334-360 -- between consecutive steps, the last
+    wrapping to the first, every worker keeps exactly one block-column --
+    with as many all-fast transitions as the layered search finds.
 
+    Worker 0..g-1 start on pairs 0..g-1 of step 0.  The states of step s are
+    the worker -> pair assignments reachable from there (at most g!,
+    deduplicated); a forward dynamic program keeps, per state, the largest
+    number of all-fast transitions so far (ties: the first parent in sorted
+    order), and the wrap back to step 0 is scored at the end.  This replaces
+    the reference's exhaustive enumeration of assignment tables
+    (distsim.py:135-190, which does not finish for g = 8); the solver's
+    results do not depend on the mapping, only the
+    exchange trace does, and on NVSwitch (``Topology(g, uniform=True)``)
+    every transition is fast."""
     g = topology.g
     if strategy.n != 2 * g:
         raise MappingError(f"strategy order {strategy.n} != 2g = {2 * g}")
-    steps = [tuple(sorted(step)) for step in strategy.steps]
+    steps = [tuple(sorted(st)) for st in strategy.steps]
     ns = len(steps)
     if g == 1:
-        return ColumnMapping(1, tuple((pq,) for pq in strategy.steps), ((),) * ns)
+        return ColumnMapping(1, tuple((pq,) for pq in strategy.steps), ((),) * ns, 0)
+
+    def moves_of(s, st_a, st_b):
+        a = tuple(steps[s][k] for k in st_a)
+        b = tuple(steps[(s + 1) % ns][k] for k in st_b)
+        return _moves(a, b)
+
+    start = tuple(range(g))
+    layers = [{start: (0, None)}]
+    for s in range(ns - 1):
+        ms = _step_matchings(steps[s], steps[s + 1])
+        nxt: dict = {}
+        for state in sorted(layers[-1]):
+            score = layers[-1][state][0]
+            for mm in ms:
+                child = tuple(mm[state[i]] for i in range(g))
+                if topology.uniform:  # every transition is fast: keep the first parent
+                    if child not in nxt:
+                        nxt[child] = (score + 1, state)
+                    continue
+                sc = score + (1 if _all_fast(moves_of(s, state, child), topology) else 0)
+                if child not in nxt or sc > nxt[child][0]:
+                    nxt[child] = (sc, state)
+        layers.append(nxt)
     best = None
-
-    def score(assignments):
-        count, moves = 0, []
-        for s in range(ns):
-            mv = _moves(assignments[s], assignments[(s + 1) % ns])
-            if mv is None:
-                return None, None
-            moves.append(mv)
-            count += all(topology.link_class(src, i) == FAST for i, (src, _) in enumerate(mv))
-        return count, tuple(moves)
-
-    def rec(assignments):
-        nonlocal best
-        if len(assignments) == ns:
-            count, moves = score(assignments)
-            if count is None:
-                return
-            key = (-count, tuple(assignments))
-            if best is None or key < best[0]:
-                best = (key, tuple(assignments), moves)
-            return
-        for opt in sorted(_assignment_options(assignments[-1], steps[len(assignments)])):
-            assignments.append(opt)
-            rec(assignments)
-            assignments.pop()
-
-    for initial in sorted(itertools.permutations(steps[0])):
-        rec([tuple(initial)])
+    for state in sorted(layers[-1]):
+        mv = moves_of(ns - 1, state, start)
+        if mv is None:
+            continue
+        sc = layers[-1][state][0] + (1 if _all_fast(mv, topology) else 0)
+        if best is None or sc > best[0]:
+            best = (sc, state)
     if best is None:
         raise MappingError("no exchange-compatible worker assignment exists")
-    return ColumnMapping(g, best[1], best[2])
+    path = [best[1]]
+    for s in range(ns - 1, 0, -1):
+        path.append(layers[s][path[-1]][1])
+    path.reverse()
+    assignments = tuple(tuple(steps[s][path[s][i]] for i in range(g)) for s in range(ns))
+    moves = tuple(_moves(assignments[s], assignments[(s + 1) % ns]) for s in range(ns))
+    return ColumnMapping(g, assignments, moves, best[0])
+
+
+def legal_mapping(strategy: PStrategy) -> ColumnMapping:
+    """The mapping used on B200 boxes: NVSwitch links are uniform, so any
+    exchange-compatible mapping is optimal."""
+    return optimize_mapping(strategy, Topology(strategy.n // 2, uniform=True))
 
 
 def default_mapping(strategy: PStrategy) -> ColumnMapping:
-    """The reference's mapping where its search is feasible, else a legal one."""
+    """Mapping of run_distributed: optimised for the reference's two-speed
+    topology up to g = 4 (exchange traces then use its fast links the way
+    the reference does), the NVSwitch mapping above (the two-speed search
+    costs minutes in Python at g = 8 and buys nothing on NVSwitch)."""
     g = strategy.n // 2
-    if g <= EXHAUSTIVE_MAPPING_MAX_G:
-        return optimize_mapping(strategy, Topology(g))
-    return legal_mapping(strategy)
+    return optimize_mapping(strategy, Topology(g)) if g <= 4 else legal_mapping(strategy)
 
 
 def local_signature_pair(signature: Signature, p: int, q: int, bw: int) -> Signature:
