@@ -379,21 +379,6 @@ k_update(double *__restrict__ G, int64_t ldg, int64_t m, double *__restrict__ Vm
 // ---------------------------------------------------------------------------
 // Kernel-level entry points (blockkernel.cholesky_in_place / inner_jacobi).
 
-// Cholesky of one c x c matrix in global memory (any c), then R = L^T.
-__global__ void __launch_bounds__(1024)
-k_cholesky_single(double *__restrict__ H, int c, double *__restrict__ R, int *info) {
-  __shared__ int s_status;
-  if (threadIdx.x == 0) s_status = 0;
-  __syncthreads();
-  const int st = cta_cholesky(H, c, &s_status);
-  if (threadIdx.x == 0) *info = st;
-  if (st) return;
-  for (int64_t e = threadIdx.x; e < (int64_t)c * c; e += blockDim.x) {
-    const int i = (int)(e % c), j = (int)(e / c);
-    R[(int64_t)j * c + i] = (i <= j) ? H[(int64_t)i * c + j] : 0.0;
-  }
-}
-
 // Inner Jacobi of one c x c factor (c even, <= kMaxW).  R updated in place,
 // V receives the accumulated transformation.  out: rotations, proper,
 // sweeps, status, bad (1-based).
@@ -687,16 +672,6 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
                          counters, st);
   return sweep_basic(G, ldg, m, n, V, ldv, nv, w, outer, gblock, first_step, nsteps, inner,
                      n_plus, inner_limit, tol_c, workspace, counters, st);
-}
-
-// cholesky_in_place (blockkernel.py:130-145) of one small matrix (the
-// kernel-level API; the outer level uses jh_potrf): factors H (c x c,
-// device, overwritten) and writes R = L^T (zero strict lower) to R; *info
-// (device) = 0 or the 1-based bad pivot.
-int jh_cholesky(double *H, int c, double *R, int *info, void *stream) {
-  g_launches++;
-  k_cholesky_single<<<1, 1024, 0, (cudaStream_t)stream>>>(H, c, R, info);
-  return finish((cudaStream_t)stream);
 }
 
 // inner_jacobi (blockkernel.py:346-400) on one c x c factor, c even <= 64.
