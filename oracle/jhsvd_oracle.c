@@ -558,7 +558,7 @@ void or_back_substitute(const double *r, int n, const double *w, int nc, double 
 int or_block_sweep(double *g, int64_t ldg, int64_t m, int64_t n, double *v, int64_t ldv,
                    int64_t nv, int w, const int32_t *outer, int nsteps, const int32_t *inner,
                    int64_t n_plus, int inner_limit, double tol_c, int shortening,
-                   int threads, int64_t *counts, int64_t *err) {
+                   int threads, int64_t *counts, int64_t *err, const int32_t *gblock) {
     int bw = w / 2;
     int64_t b = n / bw;
     int ntask = (int)(b / 2);
@@ -596,7 +596,11 @@ int or_block_sweep(double *g, int64_t ldg, int64_t m, int64_t n, double *v, int6
             }
             if (!st) {
                 for (int j = 0; j < w; j++) {
-                    int64_t gcol = (j < bw ? cp0 + j : cq0 + j - bw) + 1;  /* 1-based */
+                    /* gblock: global block index of a local block-column (sharded
+                     * solves; the signature follows the global column) */
+                    int64_t gp0 = gblock ? (int64_t)gblock[bp] * bw : cp0;
+                    int64_t gq0 = gblock ? (int64_t)gblock[bq] * bw : cq0;
+                    int64_t gcol = (j < bw ? gp0 + j : gq0 + j - bw) + 1;  /* 1-based */
                     sg[j] = gcol <= n_plus ? 1 : -1;
                 }
                 memset(vacc, 0, sizeof(double) * (size_t)w * w);

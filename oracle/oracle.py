@@ -62,7 +62,7 @@ def lib():
         L.or_safe_bounds.argtypes = [_i64, _p, _p]
         L.or_rotation.argtypes = [_d, _d, _d, _d, _p]
         L.or_block_sweep.argtypes = [_p, _i64, _i64, _i64, _p, _i64, _i64, _i32, _p, _i32,
-                                     _p, _i64, _i32, _d, _i32, _i32, _p, _p]
+                                     _p, _i64, _i32, _d, _i32, _i32, _p, _p, _p]
         L.or_block_sweep.restype = _i32
         L.or_max_threads.restype = _i32
         L.or_gen_butterfly.argtypes = [_p, _i64, _i64, _i64, _p, _i64, ctypes.c_uint64, _i32, _d]
@@ -199,9 +199,13 @@ def _cfg(cfg):
     return ns
 
 
-def block_sweep(g, v, n_plus, cfg, outer_tab, inner_tab, threads=0, nsteps=None):
+def block_sweep(g, v, n_plus, cfg, outer_tab, inner_tab, threads=0, nsteps=None, gblock=None,
+                err_out=None):
     """One block sweep (or its first ``nsteps`` p-steps) in place; returns
-    (rotations, proper).  Raises OracleError like the reference."""
+    (rotations, proper).  Raises OracleError like the reference.  ``gblock``
+    (int32 per local block-column) gives the global block index for the J
+    signature of sharded solves; with ``err_out`` (list) the failure (status,
+    1-based index, p-step, task) is appended instead of raised."""
     c = _cfg(cfg)
     m, n = g.shape
     w = c.block_width
@@ -213,10 +217,14 @@ def block_sweep(g, v, n_plus, cfg, outer_tab, inner_tab, threads=0, nsteps=None)
     tol_c = EPS * math.sqrt(w) * c.eps_factor
     vp = _ptr(v) if v is not None else None
     nv = v.shape[0] if v is not None else 0
+    gb = np.ascontiguousarray(gblock, dtype=np.int32) if gblock is not None else None
     st = lib().or_block_sweep(_ptr(g), m, m, n, vp, nv, nv, w, _ptr(tab), ns, _ptr(itab),
                               int(n_plus), c.inner_limit, tol_c,
                               0 if c.shortening == "cholesky" else 1, int(threads),
-                              _ptr(counts), _ptr(err))
+                              _ptr(counts), _ptr(err), _ptr(gb) if gb is not None else None)
+    if st and err_out is not None:
+        err_out.append((int(st), int(err[0]), int(err[1]), int(err[2])))
+        return int(counts[0]), int(counts[1])
     if st == 1 or st == 2:
         raise OracleError("rank", int(err[0]))
     if st == 3:
