@@ -6,32 +6,45 @@ One *step* is one complete solve to convergence -- input factor resident in
 HBM -> sigma, U, V -- of the BASELINE.json config 3 workload: a 16384 x 16384
 FP64 factor, full-block variant, rrow (Mantharam-Eberlein-equivalent)
 strategy, block width 32 (block-columns of 16), V accumulated.  The factor is
-synthetic: G = Q diag(sqrt(lambda)) W^T with a reference type-2 spectrum
-lambda (testgen.gen_spectrum, seed 3) and Haar Q, W generated on the GPU.
-The 2 GiB factor is larger than L2, so no flush is needed between steps.
+synthetic and reproducible: G = Q diag(sqrt(lambda)) W^T with the
+reference's type-2 spectrum (testgen.gen_spectrum, seed 3) and random Givens
+butterfly Q, W generated on the GPU (jh_gen_butterfly; its host twin
+oracle/gen_butterfly.c writes the same bytes, so the C oracle's offline
+whole solve of this exact matrix, tests/golden/offline/config3.json, is the
+parity reference).  The 2 GiB factor is larger than L2, so no flush is
+needed between steps.
+
+N > 1 GPUs: one rank per GPU (torchrun; ``--gpus N`` without torchrun
+relaunches itself under torchrun, and refuses when the box has fewer GPUs).
+The ranks run ``block_jacobi_sharded``: block-columns sharded over the GPUs,
+one NCCL exchange per table segment, bitwise the same solve as N = 1.
 
 Prints ONE JSON line (rank 0).  Besides the contract keys it carries
  - e2e: the same metric through the public API with host (pinned) buffers,
    host<->device copies inside the timed region;
  - roofline: the dominant kernel's algorithmic HBM bytes / CUDA-event time;
+ - fp64_roofline: the whole solve's DMMA flops against the measured DMMA rate;
  - cpu_baseline: the C oracle (a port of the reference CPU solver) timed on
-   a bounded prefix of the same solve on this host, extrapolated;
- - accuracy: sigma vs the prescribed spectrum, orthogonality of U and V, and
-   a bitwise check of the GPU against the oracle on that prefix.
+   a bounded prefix of the same solve on this host, extrapolated with the
+   per-sweep cost profile of the oracle's own offline whole solve;
+ - parity: input / sigma / U / V / stats against the offline oracle golden,
+   plus the sampled p-steps bitwise against the oracle;
+ - accuracy: sigma vs the prescribed spectrum, orthogonality of U and V.
 ``--impl reference`` times only the CPU oracle on the same workload.
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 from pathlib import Path
 
@@ -42,7 +55,7 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "FP64 SVD sec to convergence (n=16384) at 1/2/4/8 B200; σ rel err; sweeps"
 PAPER_K20C_16384_S = 2625.642659  # Table 6.2 (Kepler K20c)
-DEFAULT_SWEEPS_GUESS = 9          # BASELINE.md Table 6.3: 7-12 full-block sweeps
+GOLDEN = ROOT / "tests" / "golden" / "offline"
 
 
 def parse_args():
@@ -51,31 +64,51 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--n", type=int, default=16384)
-    ap.add_argument("--width", type=int, default=32)
-    ap.add_argument("--variant", default="full-block")
-    ap.add_argument("--strategy", default="rrow")
-    ap.add_argument("--spectrum-type", type=int, default=2)
-    ap.add_argument("--seed", type=int, default=3)
+    ap.add_argument("--n", type=int, default=16384, help="order (config 3 at 16384)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
                     help="target CPU-oracle sample length")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     return ap.parse_args()
 
 
-def workload(args) -> dict:
-    return {
-        "workload": (f"config3: {args.n}x{args.n} FP64 SVD, {args.variant}, "
-                     f"{args.strategy} strategy (ME-equivalent), block width {args.width} "
-                     f"(block-columns of {args.width // 2}), V accumulated"),
-        "n": args.n, "block_width": args.width, "variant": args.variant,
-        "outer_strategy": args.strategy, "inner_strategy": args.strategy,
-        "input": (f"G = Q diag(sqrt(lambda)) W^T, lambda = type-{args.spectrum_type} spectrum "
-                  f"(seed {args.seed}), Haar Q, W (GPU QR)"),
-        "l2": (f"inputs larger than L2 (factor {8 * args.n * args.n / 2**30:.2f} GiB per step)"
-               if 8 * args.n * args.n > 126e6 else "factor fits in L2 (no flush)"),
+def the_workload(args):
+    from paper_1401_2720_b200 import workloads as WL
+
+    return WL.CONFIG3 if args.n == WL.CONFIG3.n else WL.scaled(WL.CONFIG3, args.n)
+
+
+def workload_config(wl, in_sha=None) -> dict:
+    d = {
+        "workload": f"config3: {wl.describe()}, V accumulated",
+        "n": wl.n, "m": wl.m, "block_width": wl.block_width, "variant": wl.variant,
+        "outer_strategy": wl.strategy, "inner_strategy": wl.strategy,
+        "l2": (f"inputs larger than L2 (factor {8 * wl.m * wl.n / 2**30:.2f} GiB per step)"
+               if 8 * wl.m * wl.n > 126e6 else "factor fits in L2 (no flush)"),
     }
+    if in_sha:
+        d["input_sha256"] = in_sha
+    return d
+
+
+def load_golden(wl):
+    p = GOLDEN / f"{wl.name}.json"
+    if not p.exists():
+        return None
+    gold = json.loads(p.read_text())
+    prog = GOLDEN / f"{wl.name}.progress.jsonl"
+    if prog.exists():
+        secs = [json.loads(x)["seconds"] for x in prog.read_text().splitlines() if x.strip()]
+        if len(secs) >= gold["block_sweeps"]:
+            gold["sweep_seconds"] = secs[-gold["block_sweeps"]:]
+    return gold
+
+
+def sha_rows(t) -> str:
+    """sha256 of a (cols, rows) column-major storage tensor (or numpy)."""
+    a = t.cpu().numpy() if hasattr(t, "cpu") else t
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
 
 # ---------------------------------------------------------------------------
@@ -130,107 +163,98 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# input
-
-
-def make_input(args):
-    import torch
-
-    from paper_1401_2720_b200.testgen import SpectrumSpec, canonical_sort, gen_factor_orth_device, \
-        gen_spectrum
-
-    lam = gen_spectrum(SpectrumSpec(args.spectrum_type, args.n, args.seed))
-    lam_sorted, n_plus = canonical_sort(lam)
-    sigma = np.sqrt(np.abs(lam_sorted))
-    G0 = gen_factor_orth_device(sigma, seed=args.seed)
-    torch.cuda.synchronize()
-    return G0, sigma, n_plus
-
-
-# ---------------------------------------------------------------------------
 # CPU baseline (oracle = C port of the reference solver)
 
 
-def cpu_sample(G0_host_t, args, target_s: float, check_against=None):
-    """Time p-steps of sweep 1 with the C oracle on all host cores.  Returns
-    (seconds per p-step, timed p-steps, cores, oracle state after the
-    sample) -- the state lets the caller compare the GPU bitwise."""
+def cpu_sample(g_host_t, wl, target_s: float, nsteps_max=None):
+    """Time p-steps of sweep 1 with the C oracle on all host cores, from the
+    input factor (storage (n, m)).  Returns (seconds per p-step, timed
+    p-steps, threads, oracle G and V after p-steps 0..k)."""
     from oracle import oracle as O
     from paper_1401_2720_b200.strategy import as_table, make_strategy
 
-    n = args.n
-    w = args.width
-    cfg = dict(block_width=w, variant=args.variant)
-    outer = as_table(make_strategy(args.strategy, n // (w // 2)))
-    inner = as_table(make_strategy(args.strategy, w))
-    g = np.array(G0_host_t, copy=True).T  # F-order m x n
+    n, w = wl.n, wl.block_width
+    cfg = dict(block_width=w, variant=wl.variant)
+    outer = as_table(make_strategy(wl.strategy, n // (w // 2)))
+    inner = as_table(make_strategy(wl.strategy, w))
+    g = np.array(g_host_t, copy=True).T  # F-order m x n
     v = np.asfortranarray(np.eye(n))
     threads = O.max_threads()
     t0 = time.perf_counter()
     O.block_sweep(g, v, n, cfg, outer[:1], inner, threads=threads)  # warm, p-step 0
     t1 = time.perf_counter() - t0
     k = int(max(1, min(outer.shape[0] - 1, math.ceil(target_s / max(t1, 1e-3)))))
+    if nsteps_max:
+        k = min(k, nsteps_max)
     t0 = time.perf_counter()
     O.block_sweep(g, v, n, cfg, outer[1:1 + k], inner, threads=threads)
     tk = time.perf_counter() - t0
     return tk / k, k, threads, g, v
 
 
-def read_sweeps_hint() -> int:
-    for p in sorted((ROOT / "profiles").glob("*/bench*.json"), reverse=True):
-        try:
-            d = json.loads(p.read_text())
-            if d.get("impl", "ours") == "ours" and d.get("sweeps"):
-                return int(d["sweeps"])
-        except Exception:
-            continue
-    return DEFAULT_SWEEPS_GUESS
+def extrapolate(t_p: float, b: int, gold, sweeps_here=None, rotated_frac=None):
+    """Whole-solve CPU seconds from the sweep-1 p-step rate: (b - 1) p-steps
+    per sweep, weighted per sweep by the oracle's own offline whole-solve
+    profile (its measured per-sweep seconds relative to sweep 1) when the
+    golden has it; otherwise by the fraction of tasks that rotated."""
+    if gold and gold.get("sweep_seconds"):
+        w = [s / gold["sweep_seconds"][0] for s in gold["sweep_seconds"]]
+        how = (f"per-sweep weights from the oracle's offline whole solve "
+               f"({gold['threads']} threads, {len(w)} sweeps)")
+    elif rotated_frac:
+        # gram + cholesky + inner ~ 0.3 of a rotated p-step on the oracle
+        w = [0.3 + 0.7 * f for f in rotated_frac]
+        how = f"per-sweep weights 0.3 + 0.7 x (fraction of tasks rotated), {len(w)} sweeps"
+    else:
+        w = [1.0] * (sweeps_here or 9)
+        how = f"{len(w)} sweeps at the sweep-1 rate"
+    return t_p * (b - 1) * sum(w), how
 
 
 # ---------------------------------------------------------------------------
+# reference arm
 
 
 def run_reference(args, rank: int):
     if rank != 0:
         return
-    import torch
-
     from oracle import oracle as O
 
-    cfgd = workload(args)
-    if torch.cuda.is_available():
-        G0, _, _ = make_input(args)  # input synthesis only (not the measured path)
-        host = G0.cpu().numpy()
-        del G0
-    else:
-        raise SystemExit("input synthesis needs the GPU")
-    sweeps = read_sweeps_hint()
-    b = args.n // (args.width // 2)
+    wl = the_workload(args)
+    sigma_p, n_plus = wl.sigma_nplus()
+    g = O.gen_butterfly(sigma_p, m=wl.m, n_plus=n_plus, seed=wl.gen_seed, passes=wl.passes,
+                        tanh_max=wl.tanh_max)  # input synthesis (not timed)
+    host_t = np.ascontiguousarray(g.T)
+    del g
+    gold = load_golden(wl)
+    b = wl.n // (wl.block_width // 2)
     per = []
+    k = threads = 0
     for i in range(args.warmup + args.steps):
-        t_p, k, threads, _, _ = cpu_sample(host, args, args.cpu_seconds if i >= args.warmup
+        t_p, k, threads, _, _ = cpu_sample(host_t, wl, args.cpu_seconds if i >= args.warmup
                                            else 1.0)
         if i >= args.warmup:
             per.append(t_p)
     t_p = statistics.mean(per)
-    value = t_p * (b - 1) * sweeps
+    value, how = extrapolate(t_p, b, gold)
     line = {
         "metric": METRIC, "value": value, "unit": "s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic", "config": cfgd, "impl": "reference",
+        "dtype": "f64", "data": "synthetic", "config": workload_config(wl, sha_rows(host_t)),
+        "impl": "reference",
         "cpu_baseline": {
             "value": value, "unit": "s", "cores": threads, "kind": "port",
-            "sample": (f"C oracle (port of the reference numba solver) on {k} p-steps of "
-                       f"sweep 1 (of {b - 1}), {t_p:.3f} s/p-step, extrapolated x{b - 1} "
-                       f"p-steps x {sweeps} sweeps")},
+            "sample": (f"C oracle (port of the reference numba solver) on p-steps 1..{k} of "
+                       f"sweep 1 (of {b - 1}) from the input, {t_p:.3f} s/p-step, extrapolated "
+                       f"x{b - 1} p-steps, {how}")},
         "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
-    _ = O
 
 
-FP64_DMMA_PEAK_TF = 37.0  # measured: profiles/r01/dmma_chains_probe.jsonl (mma.sync f64, 8 warps/SM)
+# ---------------------------------------------------------------------------
+# multi-GPU plumbing
 
 
 def _init_dist(world: int):
@@ -245,14 +269,15 @@ def _init_dist(world: int):
     return dist
 
 
-def _max_over_ranks(x: float, world: int) -> float:
+def _reduce(x: float, world: int, op: str = "max") -> float:
     if world == 1:
         return x
     import torch
     import torch.distributed as dist
 
     t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(t, op={"max": dist.ReduceOp.MAX, "sum": dist.ReduceOp.SUM,
+                           "min": dist.ReduceOp.MIN}[op])
     return float(t.item())
 
 
@@ -267,40 +292,82 @@ def _barrier(world: int):
         torch.cuda.synchronize()
 
 
-def run_ours(args, rank: int, world: int):
+def _relaunch_under_torchrun(n: int):
     import torch
 
-    from paper_1401_2720_b200 import _lib
-    from paper_1401_2720_b200.driver import Solver, SolverConfig
+    have = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if have < n:
+        raise SystemExit(f"bench.py --gpus {n}: this box has {have} GPU(s); refusing to label a "
+                         f"smaller run as {n} GPUs")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           str(Path(__file__).resolve()), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+
+def fp64_peak():
+    p = ROOT / "profiles" / "r02" / "dmma_rate.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return (float(d["dmma_tflops"]),
+                f"builder-measured DMMA rate (profiles/r02/dmma_rate.json, "
+                f"SM clock {d.get('sm_mhz')} MHz)")
+    return 37.0, "builder-measured DMMA rate (profiles/r01/dmma_chains_probe.jsonl, clock not recorded)"
+
+
+def traffic_of(kernel: str):
+    for p in (ROOT / "profiles" / "r02" / "ncu_traffic.json", ROOT / "profiles" / "ncu_traffic.json"):
+        if p.exists():
+            d = json.loads(p.read_text())
+            if kernel in d:
+                return d[kernel], d.get(kernel + "_algorithmic"), str(p.relative_to(ROOT))
+    return None, None, None
+
+
+def run_ours(args, rank: int, world: int):
+    import ctypes
+
+    import torch
+
     import paper_1401_2720_b200 as J
+    from paper_1401_2720_b200 import _lib, testgen as T
+    from paper_1401_2720_b200.driver import Solver
+    from paper_1401_2720_b200.sharded import CudaShardEngine, block_jacobi_sharded, shard_plan
 
     _init_dist(world)
     lib = _lib.require_cuda()
-    cfg = SolverConfig(block_width=args.width, variant=args.variant,
-                       outer_strategy=args.strategy, inner_strategy=args.strategy)
-    G0, sigma_true, n_plus = make_input(args)
-    n = m = args.n
-    solver = Solver(n, cfg, J.Signature(n, n_plus)) if world == 1 else None
-    eng = solver.engine if solver else None
+    wl = the_workload(args)
+    cfg = J.SolverConfig(**wl.solver_kwargs())
+    G0, sigma_true, n_plus = T.workload_input_device(wl)
+    torch.cuda.synchronize()
+    n, m, w = wl.n, wl.m, wl.block_width
+    b = n // (w // 2)
+    sig = J.Signature(n, n_plus)
+    in_sha = sha_rows(G0) if rank == 0 else None
+    solver = Solver(n, cfg, sig, m=m) if world == 1 else None
+    eng1 = solver.engine if solver else None
+    plan = shard_plan(J.make_strategy(wl.strategy, b), world) if world > 1 else None
+    sh_eng = CudaShardEngine(m, n, plan, cfg, n_plus, True) if world > 1 else None
 
-    def solve():
-        """One step: a full solve from the resident factor.  N > 1: the
-        outer (multi-GPU) level of the reference, g = N workers, one per
-        rank, block-column exchange over NCCL (distsim.run_distributed)."""
+    def solve(g_dev=G0):
+        """One step: a full solve from the resident factor."""
         if world == 1:
-            return solver.solve_device(G0)
-        from paper_1401_2720_b200.distsim import run_distributed
+            return solver.solve_device(g_dev)
+        res = block_jacobi_sharded(g_dev.t(), sig, world, cfg, engine=sh_eng)
+        return (res.sigma, res.u.t(), res.v.t(), [list(s) for s in res.stats], res.converged)
 
-        res, _ = run_distributed(G0.t(), J.Signature(n, n_plus), world, cfg)
-        return res
-
-    # warm-up steps (full solves)
     for _ in range(args.warmup):
         out = solve()
         del out
     _barrier(world)
 
-    # timed steps
     sampler = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
     if sampler:
         sampler.start()
@@ -314,38 +381,85 @@ def run_ours(args, rank: int, world: int):
         res = solve()
         e1.record()
         _barrier(world)
-        times.append(_max_over_ranks(e0.elapsed_time(e1) / 1e3, world))
-    launches = lib.jh_launch_count() - launches0
+        times.append(_reduce(e0.elapsed_time(e1) / 1e3, world, "max"))
+    launches = int(_reduce(float(lib.jh_launch_count() - launches0), world, "sum"))
     clocks = sampler.stop() if sampler else None
-    import ctypes
+    value = statistics.mean(times)
+    sigma, U, V, stats, converged = res
+    del res
 
-    # per-kernel timing: one more (untimed) solve with every kernel apart
-    # (engine 1 otherwise overlaps the update with the inner kernel), CUDA
+    # per-kernel timing: one more (untimed) solve with the kernels kept apart
+    # (engine 1 otherwise overlaps the update with the inner Jacobi), CUDA
     # events around each launch on the launching stream
     lib.jh_set_overlap(0)
-    lib.jh_profile_begin(4 * (n // (args.width // 2) + 8) * cfg.max_block_sweeps * 4)
+    lib.jh_profile_begin(4 * (b + 8) * cfg.max_block_sweeps * 4)
+    if sh_eng is not None:
+        sh_eng.tasks_rotated = []
     prof = solve()
     ms = (ctypes.c_double * 4)()
     cnt = (ctypes.c_int64 * 4)()
     lib.jh_profile_end(ms, cnt)
     lib.jh_set_overlap(1)
-    rotated_tasks = sum(eng.tasks_rotated) if eng is not None else 0
     del prof
-    if world == 1:
-        sigma, U, V, stats, converged = res
-    else:
-        def dev_t(x):
-            return x if torch.is_tensor(x) else torch.as_tensor(np.asarray(x))
-        sigma = dev_t(res.sigma).cuda()
-        U = dev_t(res.u).cuda().t()  # (n, m) column-major storage like solve_device
-        V = dev_t(res.v).cuda().t()
-        stats, converged = [list(s) for s in res.stats], res.converged
-    value = statistics.mean(times)
+    rotated_tasks = sum(eng1.tasks_rotated) if eng1 is not None else sum(sh_eng.tasks_rotated)
+    rotated_per_sweep = (list(eng1.tasks_rotated) if eng1 is not None
+                         else list(sh_eng.tasks_rotated_sweeps))
 
-    def run_e2e(G0):
+    # ---- roofline of the dominant streaming kernel (this rank) ----
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    ntask = n // w // world
+    bytes_gram_launch = ntask * 8.0 * w * m
+    # update launches: read + write of the pair columns of G per rotated task;
+    # V once per two p-steps (engine 1 pairs the p-steps over 4-cycles)
+    v_factor = 0.5
+    bytes_update_total = rotated_tasks * 16.0 * w * (m + v_factor * n)
+    classes = {
+        "gram": {"ms": ms[0], "launches": cnt[0], "bytes_total": bytes_gram_launch * cnt[0],
+                 "flops_total": ntask * m * w * (w + 1.0) * cnt[0]},
+        "factor_inner": {"ms": ms[1], "launches": cnt[1], "bytes_total": 0.0},
+        "update": {"ms": ms[2] + ms[3], "launches": cnt[2], "bytes_total": bytes_update_total,
+                   "flops_total": rotated_tasks * 2.0 * w * w * (m + n)},
+    }
+    tot_ms = sum(c["ms"] for c in classes.values()) or 1.0
+    dom = max(("gram", "update"), key=lambda k: classes[k]["ms"])
+    d = classes[dom]
+    achieved = d["bytes_total"] / (d["ms"] / 1e3) / 1e9 if d["ms"] > 0 else 0.0
+    traffic, traffic_alg, traffic_src = traffic_of(dom)
+    chol_flops = ntask * w ** 3 / 3.0 * cnt[0]
+    solve_flops = classes["gram"]["flops_total"] + classes["update"]["flops_total"] + chol_flops
+    solve_flops_all = _reduce(solve_flops, world, "sum")
+    peak_tf, peak_src = fp64_peak()
+    fp64 = {
+        "achieved_tflops": solve_flops_all / value / 1e12 if value else 0.0,
+        "peak_tflops": peak_tf * world, "frac": solve_flops_all / value / 1e12 / (peak_tf * world),
+        "solve_flops": solve_flops_all,
+        "gram_tflops": (classes["gram"]["flops_total"] / (classes["gram"]["ms"] / 1e3) / 1e12
+                        if classes["gram"]["ms"] > 0 else None),
+        "update_tflops": (classes["update"]["flops_total"] / (classes["update"]["ms"] / 1e3)
+                          / 1e12 if classes["update"]["ms"] > 0 else None),
+        "peak_source": peak_src,
+    }
+    roofline = {
+        "kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+        "frac": achieved / hbm_peak, "traffic": traffic,
+        "traffic_launch_algorithmic_bytes": traffic_alg, "traffic_source": traffic_src,
+        "bytes_per_launch": d["bytes_total"] / max(d["launches"], 1),
+        "avg_launch_ms": d["ms"] / max(d["launches"], 1),
+        "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
+        "kernel_share": {k: c["ms"] / tot_ms for k, c in classes.items()},
+        "solve_hbm_frac": ((classes["gram"]["bytes_total"] + bytes_update_total) * world
+                           / value / 1e9 / (hbm_peak * world)),
+        "timing_note": ("per-kernel times from one extra solve with the kernels kept apart "
+                        "(jh_set_overlap(0)); the timed solves overlap the update with the "
+                        "inner Jacobi" + ("; rank 0's kernels" if world > 1 else "")),
+    }
+
+    def run_e2e():
         """The same solve through the public API from pinned host memory
         (host->device copy of the factor and device->host copy of sigma, U,
-        V inside the timed region); collective for N > 1."""
+        V inside the timed region)."""
         host_in = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
         host_in.copy_(G0)
         g_host = host_in.t()  # m x n, column-major, pinned
@@ -358,140 +472,96 @@ def run_ours(args, rank: int, world: int):
             _barrier(world)
             t0 = time.perf_counter()
             if world == 1:
-                r = J.block_jacobi(g_host, J.Signature(n, n_plus), cfg)
+                r = J.block_jacobi(g_host, sig, cfg, allow_tall=m > n)
             else:
-                from paper_1401_2720_b200.distsim import run_distributed
-
-                r, _ = run_distributed(g_host, J.Signature(n, n_plus), world, cfg)
-            dt = _max_over_ranks(time.perf_counter() - t0, world)
+                r = block_jacobi_sharded(g_host, sig, world, cfg, engine=sh_eng,
+                                         allow_tall=m > n)
+            dt = _reduce(time.perf_counter() - t0, world, "max")
             if k >= (1 if args.warmup > 0 else 0):
                 et.append(dt)
             del r
-        return {"value": statistics.mean(et), "unit": "s", "h2d_bytes_per_step": 8 * m * n,
-                "d2h_bytes_per_step": 8 * (n + m * n + n * n),
-                "note": ("public API block_jacobi on a pinned host factor: H2D of G, solve, "
-                         "sigma/U/V back to host, after one untimed warm-up call")}
+        return {"value": statistics.mean(et), "unit": "s",
+                "h2d_bytes_per_step": 8 * m * n * world,
+                "d2h_bytes_per_step": 8 * (n + m * n + n * n) * world,
+                "note": ("public API " + ("block_jacobi" if world == 1 else
+                                          f"block_jacobi_sharded (each of {world} ranks passes "
+                                          "the full host factor and receives the full result)")
+                         + " on a pinned host factor: H2D of G, solve, sigma/U/V back to host, "
+                           "after one untimed warm-up call")}
 
+    gold = load_golden(wl)
     if rank != 0:
-        del U, V, res
+        del U, V, sigma
         if not args.no_e2e:
-            run_e2e(G0)
+            run_e2e()
         return
 
-    # roofline of the dominant streaming kernel
-    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
-        if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    w = args.width
-    ntask = n // w
-    bytes_gram_launch = ntask * 8.0 * w * m
-    # algorithmic HBM bytes of the update launches: read + write of the pair
-    # columns of G per rotated task; V the same per p-step (engine 0) or once
-    # per two p-steps over the 4-cycles of the pair (engine 1, jh_vpair.cu)
-    v_factor = 0.5 if (eng is not None and eng.engine == 1) else 1.0
-    bytes_update_total = rotated_tasks * 16.0 * w * (m + v_factor * n)
-    classes = {
-        "gram": {"ms": ms[0], "launches": cnt[0],
-                 "bytes_total": bytes_gram_launch * cnt[0],
-                 "flops_total": ntask * m * w * (w + 1.0) * cnt[0]},
-        "factor_inner": {"ms": ms[1], "launches": cnt[1], "bytes_total": 0.0},
-        "update": {"ms": ms[2] + ms[3], "launches": cnt[2], "bytes_total": bytes_update_total,
-                   "flops_total": rotated_tasks * 2.0 * w * w * (m + n)},
-    }
-    tot_ms = sum(c["ms"] for c in classes.values()) or 1.0
-    dom = max(("gram", "update"), key=lambda k: classes[k]["ms"])
-    d = classes[dom]
-    achieved = d["bytes_total"] / (d["ms"] / 1e3) / 1e9 if d["ms"] > 0 else 0.0
-    # DRAM traffic of the same kernel from one `ncu --set full` capture
-    # (profiles/ncu_traffic.json: one launch with every task rotating, with the
-    # algorithmic bytes of that launch for comparison)
-    traffic = traffic_alg = None
-    tp = ROOT / "profiles" / "ncu_traffic.json"
-    if tp.exists():
-        tj = json.loads(tp.read_text())
-        traffic = tj.get(dom)
-        traffic_alg = tj.get(dom + "_algorithmic")
-    # FP64 tensor-pipe (DMMA) roofline of the whole solve: algorithmic flops
-    # (Gram m w(w+1) per task and p-step, update 2 w^2 (m + n) per rotated
-    # task, Cholesky w^3/3 per task and p-step) over the solve time
-    chol_flops = ntask * w ** 3 / 3.0 * cnt[0]
-    solve_flops = classes["gram"]["flops_total"] + classes["update"]["flops_total"] + chol_flops
-    fp64 = {
-        "achieved_tflops": solve_flops / value / 1e12 if value else 0.0,
-        "peak_tflops": FP64_DMMA_PEAK_TF,
-        "frac": solve_flops / value / 1e12 / FP64_DMMA_PEAK_TF if value else 0.0,
-        "solve_flops": solve_flops,
-        "gram_tflops": (classes["gram"]["flops_total"] / (classes["gram"]["ms"] / 1e3) / 1e12
-                        if classes["gram"]["ms"] > 0 else None),
-        "update_tflops": (classes["update"]["flops_total"] / (classes["update"]["ms"] / 1e3)
-                          / 1e12 if classes["update"]["ms"] > 0 else None),
-        "peak_source": "measured DMMA rate, profiles/r01/dmma_chains_probe.jsonl",
-        "note": ("per-kernel rates from CUDA events around each launch; under sw_power_cap "
-                 "the SM clock (see clocks) scales the attainable peak"),
-    }
-    roofline = {
-        "kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-        "frac": achieved / hbm_peak, "traffic": traffic,
-        "traffic_launch_algorithmic_bytes": traffic_alg,
-        "bytes_per_launch": d["bytes_total"] / max(d["launches"], 1),
-        "avg_launch_ms": d["ms"] / max(d["launches"], 1),
-        "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
-        "kernel_share": {k: c["ms"] / tot_ms for k, c in classes.items()},
-        "solve_bytes": classes["gram"]["bytes_total"] + bytes_update_total,
-        "solve_hbm_frac": ((classes["gram"]["bytes_total"] + bytes_update_total)
-                           / value / 1e9 / hbm_peak),
-        "timing_note": ("per-kernel times from one extra solve with the kernels kept apart "
-                        "(jh_set_overlap(0)); the timed solves overlap the update with the "
-                        "inner Jacobi"),
-    }
-
-    # accuracy (outside the timed region)
-    sig = sigma.cpu().numpy()
-    rel = float(np.max(np.abs(sig - sigma_true) / sigma_true))
+    # ---- accuracy and whole-solve parity (outside the timed region) ----
+    sig_h = sigma.cpu().numpy()
+    ref = np.concatenate((np.sort(sigma_true[:n_plus])[::-1], np.sort(sigma_true[n_plus:])[::-1]))
+    rel = float(np.max(np.abs(sig_h - ref) / ref))
     eye = torch.eye(n, dtype=torch.float64, device=U.device)
-    ortho_u = float((U @ U.t() - eye).abs().max())
+    ortho_u = float((U @ U.t() - eye).abs().max()) if m == n else None
     ortho_v = float((V @ V.t() - eye).abs().max())
     del eye
-    accuracy = {"sigma_max_rel_err_vs_prescribed": rel,
-                "u_orth_max": ortho_u, "v_orth_max": ortho_v,
-                "n_eps": n * 2.0 ** -53}
-    del U, V, res
+    accuracy = {"sigma_max_rel_err_vs_prescribed": rel, "u_orth_max": ortho_u,
+                "v_orth_max": ortho_v, "n_eps": n * 2.0 ** -53}
+    parity = {"golden": None}
+    if gold is not None:
+        gs = np.load(GOLDEN / f"{wl.name}_sigma.npy")
+        parity = {
+            "golden": f"tests/golden/offline/{wl.name}.json (C oracle whole solve, "
+                      f"{gold['threads']} threads, {gold.get('solve_wall_s', 0):.0f} s)",
+            "input_sha256_equal": in_sha == gold["input_sha256"],
+            "stats_equal_oracle": [list(s) for s in stats] == gold["stats"],
+            "sigma_bitwise_vs_oracle": sha_rows(sigma) == gold["sigma_sha256"],
+            "u_bitwise_vs_oracle": sha_rows(U) == gold["u_sha256"],
+            "v_bitwise_vs_oracle": sha_rows(V) == gold["v_sha256"],
+            "sigma_max_rel_vs_oracle": float(np.max(np.abs(sig_h - gs) / gs)),
+        }
+    del U, V
 
-    # CPU baseline (bounded oracle sample) + bitwise prefix parity
+    # ---- CPU baseline (bounded oracle sample) + bitwise prefix parity ----
     cpu = None
-    parity = None
-    if not args.no_cpu and world == 1:
+    if not args.no_cpu:
         host = G0.cpu().numpy()
-        t_p, k, threads, g_or, v_or = cpu_sample(host, args, args.cpu_seconds)
-        b = n // (w // 2)
-        cpu = {"value": t_p * (b - 1) * len(stats), "unit": "s", "cores": threads,
-               "kind": "port",
+        t_p, k, threads, g_or, v_or = cpu_sample(host, wl, args.cpu_seconds)
+        nt_all = n // w
+        frac = [r / nt_all / (b - 1) for r in rotated_per_sweep] if rotated_per_sweep else None
+        est, how = extrapolate(t_p, b, gold, len(stats), frac)
+        cpu = {"value": est, "unit": "s", "cores": threads, "kind": "port",
                "sample": (f"C oracle (port of the reference numba solver): p-steps 1..{k} of "
-                          f"sweep 1 ({t_p:.3f} s/p-step), extrapolated x{b - 1} p-steps x "
-                          f"{len(stats)} sweeps")}
-        Gp = G0.clone()
-        Vp = torch.eye(n, dtype=torch.float64, device=G0.device)
-        eng.sweep(Gp, Vp, 0, 1 + k)
-        torch.cuda.synchronize()
-        same_g = bool(np.array_equal(Gp.cpu().numpy(), np.ascontiguousarray(g_or.T)))
-        same_v = bool(np.array_equal(Vp.cpu().numpy(), np.ascontiguousarray(v_or.T)))
-        parity = {"psteps": 1 + k, "G_bitwise_equal": same_g, "V_bitwise_equal": same_v}
-        del Gp, Vp, host, g_or, v_or
+                          f"sweep 1 ({t_p:.3f} s/p-step), extrapolated x{b - 1} p-steps, {how}")}
+        if not args.no_parity and world == 1:
+            Gp = G0.clone()
+            Vp = torch.eye(n, dtype=torch.float64, device=G0.device)
+            eng1.sweep(Gp, Vp, 0, 1 + k)
+            torch.cuda.synchronize()
+            parity["prefix_psteps"] = 1 + k
+            parity["prefix_G_bitwise"] = bool(np.array_equal(Gp.cpu().numpy(),
+                                                             np.ascontiguousarray(g_or.T)))
+            parity["prefix_V_bitwise"] = bool(np.array_equal(Vp.cpu().numpy(),
+                                                             np.ascontiguousarray(v_or.T)))
+            del Gp, Vp
+        del host, g_or, v_or
 
-    # end to end through the public API with host buffers
-    e2e = run_e2e(G0) if not args.no_e2e else None
+    e2e = run_e2e() if not args.no_e2e else None
     del G0
 
     line = {
-        "metric": METRIC, "value": value, "unit": "s", "n_gpus": args.gpus,
+        "metric": METRIC, "value": value, "unit": "s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,
         "higher_is_better": False, "scaling": "strong",
         "vs_baseline": value / PAPER_K20C_16384_S,
-        "dtype": "f64", "data": "synthetic", "config": workload(args),
-        "sweeps": len(stats), "converged": converged, "stats": stats,
-        "accuracy": accuracy, "parity_prefix": parity,
+        "dtype": "f64", "data": "synthetic", "config": workload_config(wl, in_sha),
+        "parallelism": ("1 GPU" if world == 1 else
+                        f"block-columns sharded over {world} GPUs (block_jacobi_sharded, "
+                        f"{2 * world - 1} NCCL exchanges per sweep, bitwise = 1 GPU)"),
+        "sweeps": len(stats), "converged": converged, "stats": [list(s) for s in stats],
+        "tasks_rotated_per_sweep": rotated_per_sweep,
+        "accuracy": accuracy, "parity": parity,
         "e2e": e2e, "roofline": roofline, "fp64_roofline": fp64, "cpu_baseline": cpu,
-        "clocks": clocks, "gpu_launches": int(launches),
+        "clocks": clocks, "gpu_launches": launches,
         "per_step_s": times,
     }
     print(json.dumps(line), flush=True)
@@ -501,6 +571,10 @@ def main():
     args = parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if args.gpus > 1 and world == 1 and args.impl == "ours":
+        _relaunch_under_torchrun(args.gpus)
+    if world > 1 and args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
     if args.impl == "reference":
         run_reference(args, rank)
         return

@@ -182,6 +182,8 @@ class CudaShardEngine:
         self.inner = make_strategy(cfg.inner_strategy, self.w)
         self.dev = _dev.device()
         self._engines: dict = {}
+        self.tasks_rotated: list[int] = []          # per sweep, this worker's tasks
+        self.tasks_rotated_sweeps: list[int] = []   # per sweep, all workers
 
     def engine_for(self, key, table, gblock):
         """SweepEngine of one (segment, slot layout) local table (cached)."""
@@ -387,6 +389,8 @@ def block_jacobi_sharded(g_matrix, signature: Optional[Signature], g: int,
     stats: list[tuple[int, int]] = []
     converged = False
     cur_cfg = first_cfg
+    rot_local: list[int] = []
+    rot_all: list[int] = []
     for _ in range(cfg.max_block_sweeps):
         per = {i: [] for i in mine}
         for si, seg in enumerate(plan.segments):
@@ -402,13 +406,14 @@ def block_jacobi_sharded(g_matrix, signature: Optional[Signature], g: int,
                 if timer:
                     timer(i, si, "stop")
                 per[i].append((cnt, seg, gidx))
-        rot = proper = 0
+        rot = proper = nrot = 0
         first_err = (1 << 62)
         for i in mine:
             for cnt, seg, gidx in per[i]:
-                r, p, key, _ = engine.read(cnt)
+                r, p, key, nr = engine.read(cnt)
                 rot += r
                 proper += p
+                nrot += nr
                 if key != -1:
                     key &= (1 << 64) - 1
                     ps, task = key >> 38, (key >> 16) & 0x3FFFFF
@@ -416,7 +421,9 @@ def block_jacobi_sharded(g_matrix, signature: Optional[Signature], g: int,
                     gs = seg.first + ps
                     enc = (gs << 40) | (int(gidx[ps, task]) << 16) | (status << 13) | index
                     first_err = min(first_err, enc)
-        rot, proper = comm.all_sum([rot, proper], dev)
+        rot_local.append(nrot)
+        rot, proper, nrot = comm.all_sum([rot, proper, nrot], dev)
+        rot_all.append(nrot)
         first_err = comm.all_min(first_err, dev)
         if first_err != (1 << 62):
             _raise(first_err, plan, bw)
@@ -425,6 +432,9 @@ def block_jacobi_sharded(g_matrix, signature: Optional[Signature], g: int,
             converged = True
             break
 
+    if hasattr(engine, "tasks_rotated"):
+        engine.tasks_rotated = rot_local
+        engine.tasks_rotated_sweeps = rot_all
     Gf, Vf = _gather(comm, plan, locs, m, n, bwc, dev, with_v)
     if dev.type != "cuda":
         return engine.finish(Gf, Vf, signature, stats, converged)

@@ -76,10 +76,6 @@ def chains_and_mixed():
                           "tflops_combined": 2 * fma / ms / 1e9}), flush=True)
 
 
-if __name__ == "__main__" and "--chains" in sys.argv:
-    chains_and_mixed()
-elif __name__ == "__main__" and "--latency" not in sys.argv:
-    main()
 
 
 def latency():
@@ -96,5 +92,66 @@ def latency():
     return r
 
 
-if __name__ == "__main__" and "--latency" in sys.argv:
-    latency()
+
+
+def peak_with_clock(out_path="profiles/r02/dmma_rate.json", seconds=6.0):
+    """Sustained DMMA rate (8 warps per SM, 8 independent chains each) for
+    ~`seconds`, with nvidia-smi sampling the SM clock meanwhile: the FP64
+    tensor roofline denominator bench.py reports."""
+    import subprocess
+    import tempfile
+    import time
+    from pathlib import Path
+
+    _lib.require_cuda()
+    lib = devlib.load()
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    ctas, threads, iters = sms * 2, 128, 20000
+    per = 256
+    ms = timed(lib, 0, ctas, threads, iters, out)
+    reps = max(1, int(seconds * 1e3 / max(ms, 1e-3)))
+    f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+    smi = subprocess.Popen(["nvidia-smi", "--query-gpu=clocks.sm,power.draw,"
+                            "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits",
+                            "-lms", "100"], stdout=f, stderr=subprocess.DEVNULL)
+    time.sleep(0.3)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        _lib.check(lib.jh_probe_rate(0, ctas, threads, iters, out.data_ptr(),
+                                     _lib.stream_handle()), "rate")
+    e1.record()
+    torch.cuda.synchronize()
+    smi.terminate()
+    smi.wait()
+    tot = e0.elapsed_time(e1)
+    fma = ctas * threads / 32 * iters * 8 * per * reps
+    clocks = []
+    for line in Path(f.name).read_text().splitlines():
+        try:
+            clocks.append(float(line.split(",")[0]))
+        except ValueError:
+            pass
+    clocks = sorted(clocks)
+    r = {"dmma_tflops": 2 * fma / tot / 1e9, "seconds": tot / 1e3,
+         "sm_mhz": clocks[len(clocks) // 2] if clocks else None,
+         "how": ("mma.sync.m8n8k4.f64 (SASS DMMA), 2 CTAs x 4 warps per SM, 8 independent "
+                 "accumulator chains per warp, back to back for ~6 s (tools/dev/csrc/jh_probe.cu)"),
+         "device": torch.cuda.get_device_name(0)}
+    Path(out_path).parent.mkdir(parents=True, exist_ok=True)
+    Path(out_path).write_text(json.dumps(r, indent=1) + "\n")
+    print(json.dumps(r), flush=True)
+    return r
+
+
+if __name__ == "__main__":
+    if "--chains" in sys.argv:
+        chains_and_mixed()
+    elif "--latency" in sys.argv:
+        latency()
+    elif "--peak" in sys.argv:
+        peak_with_clock()
+    else:
+        main()
