@@ -377,7 +377,10 @@ union MixSmem {
   VpSmem v;
 };
 
-__global__ void __launch_bounds__(160, 2) k_update_mix(MixArgs a) {
+#ifndef JH_MIX_MINB
+#define JH_MIX_MINB 2
+#endif
+__global__ void __launch_bounds__(160, JH_MIX_MINB) k_update_mix(MixArgs a) {
   extern __shared__ __align__(128) unsigned char smraw[];
   MixSmem &S = *reinterpret_cast<MixSmem *>(smraw);
   const int N = a.nG + a.nV, bid = blockIdx.x;
