@@ -3,7 +3,8 @@
 // (blockkernel.py:110-127), then the inner sweeps -- the pairs' dot products
 // and rotation parameters by w/2 lanes of warp 0, R applied by all threads
 // one pair at a time, V' applied by warps 1-3 one inner p-step behind
-// (blockkernel.py:278-334).
+// (blockkernel.py:278-334).  For w = 32 and many tasks per SM the
+// register-resident variant (jh_inner8.cu) runs instead.
 #include "jh_inner5.cuh"
 #include "jh_kernels.h"
 
@@ -60,6 +61,18 @@ void launch_inner5(const double *Hbuf, double *Vbuf, int64_t *trot, const int32_
                    int ntask, int w, int64_t n_plus, const int32_t *inner, int inner_limit,
                    double tol_c, unsigned long long *counters, int pstep, cudaStream_t st,
                    bool from_r, int64_t *done, int64_t epoch, const int32_t *gblock) {
+#ifndef JH_INNER8
+#define JH_INNER8 1
+#endif
+  // the register-resident kernel wins when the SMs hold several tasks each
+  // (throughput: 1.80 vs 1.82 ms per p-step at 512 tasks), the shared-memory
+  // one when tasks run nearly alone (latency: 0.186 vs 0.203 ms per inner
+  // launch at 64 tasks; tools/worker_profile.py, profiles/r02/README.md)
+  if (JH_INNER8 && inner8_ok(w) && ntask > 2 * sm_count()) {
+    launch_inner8(Hbuf, Vbuf, trot, pairs, ntask, n_plus, inner, inner_limit, tol_c, counters,
+                  pstep, st, from_r, done, epoch, gblock);
+    return;
+  }
   if (w == 16)
     launch_inner5_t<16>(Hbuf, Vbuf, trot, pairs, ntask, n_plus, inner, inner_limit, tol_c,
                         counters, pstep, st, from_r, done, epoch, gblock);

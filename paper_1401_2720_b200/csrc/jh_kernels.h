@@ -40,6 +40,13 @@ void launch_inner5(const double *Hbuf, double *Vbuf, int64_t *trot, const int32_
                    bool from_r = false, int64_t *done = nullptr, int64_t epoch = 0,
                    const int32_t *gblock = nullptr);
 
+// register-resident variant for w = 32 (jh_inner8.cu), same arguments
+bool inner8_ok(int w);
+void launch_inner8(const double *Hbuf, double *Vbuf, int64_t *trot, const int32_t *pairs,
+                   int ntask, int64_t n_plus, const int32_t *inner, int inner_limit,
+                   double tol_c, unsigned long long *counters, int pstep, cudaStream_t st,
+                   bool from_r, int64_t *done, int64_t epoch, const int32_t *gblock);
+
 // ---- QR peel-off shortening of every task of a p-step (jh_qr.cu): Rbuf[task] =
 // R (w x w, column-major) of the pair [Gp Gq]; w even <= 32, m % w == 0
 bool qr_ok(int w, int64_t m);

@@ -524,7 +524,10 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
   // Grams of p-step s+1 in the update launch of p-step s: on for G of at
   // most 2^26 entries (n = 8192: 0.626 vs 0.649 ms per p-step), off above
   // (16384^2: 1.86 vs 1.83 ms per p-step)
-  const bool gmix = m * n <= (int64_t(1) << 26) && w == 32 && nsteps > 1;
+#ifndef JH_GMIX_LOG2
+#define JH_GMIX_LOG2 26
+#endif
+  const bool gmix = m * n <= (int64_t(1) << JH_GMIX_LOG2) && w == 32 && nsteps > 1;
   if (gmix) {
     cudaMemsetAsync(gcnt, 0, sizeof(int64_t) * ntask, st);
     launch_colpos(outer + (int64_t)first_step * ntask * 2, nsteps, ntask, b, colpos, st);
