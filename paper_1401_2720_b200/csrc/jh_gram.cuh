@@ -1,6 +1,6 @@
 // DMMA Gram-tile device code shared by the Gram kernel (jh_tiles.cu) and
-// the dataflow kernel (jh_dataflow.cu): staged 64-row chunks of a block pair
-// (column stride kLd) are consumed by NW warps, each owning the lower 8x8
+// the Gram CTAs of the engine-1 update launch (jh_vpair.cu): staged 64-row
+// chunks of a block pair (column stride kLd) are consumed by NW warps, each owning the lower 8x8
 // tiles i == WARP (mod NW); every tile is one in-order DMMA chain over the
 // rows (see jh_dmma.cuh for why that is bitwise the reference's fma chain).
 #pragma once
