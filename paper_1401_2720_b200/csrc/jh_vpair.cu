@@ -360,6 +360,7 @@ struct MixArgs {
   VpArgs vp[2];
   int k0[2], kstep[2], nk[2];
   int nsrc, nV;
+  int vfirst;  // V items placed before the interleaved G / V items
   // Gram items of the next p-step at the end of the grid (nGr of them)
   int nGr;
   const int32_t *pairs_next;  // pair table row of p-step s+1
@@ -407,15 +408,17 @@ __global__ void __launch_bounds__(160, JH_MIX_MINB) k_update_mix(MixArgs a) {
                S.g.full, S.g.empty);
     return;
   }
-  // item order: V items spread evenly among the G items, or (JH_VORDER 1)
-  // all V items first -- they do not wait for the inner kernel
+  // item order: the first a.vfirst CTAs are V items -- they do not wait for
+  // the inner kernel, so in a programmatic launch they run beside its
+  // CTAs -- then the remaining V items spread evenly among the G items
   int64_t v0, v1;
-  if (kMixVOrder == 1) {
-    v0 = bid < a.nV ? bid : a.nV;
-    v1 = bid < a.nV ? bid + 1 : a.nV;
+  if (bid < a.vfirst) {
+    v0 = bid;
+    v1 = bid + 1;
   } else {
-    v0 = (int64_t)bid * a.nV / N;
-    v1 = (int64_t)(bid + 1) * a.nV / N;
+    const int64_t b2 = bid - a.vfirst, n2 = N - a.vfirst, nv2 = a.nV - a.vfirst;
+    v0 = a.vfirst + b2 * nv2 / n2;
+    v1 = a.vfirst + (b2 + 1) * nv2 / n2;
   }
   if (v1 == v0) {
     const int i = bid - (int)v0;
@@ -558,6 +561,10 @@ void launch_update_mix(double *G, int64_t ldg, int64_t m, const int32_t *pairs, 
     a.Hn = Hgram;
   }
   if (a.nG + a.nV + a.nGr == 0) return;
+#ifndef JH_VFIRST_PCT
+#define JH_VFIRST_PCT 0
+#endif
+  a.vfirst = kMixVOrder == 1 ? a.nV : (done ? (int)((int64_t)a.nV * JH_VFIRST_PCT / 100) : 0);
   const size_t smem = sizeof(MixSmem);
   ensure_smem((const void *)k_update_mix, (int)smem);
   if (!done) {
