@@ -494,6 +494,7 @@ def run_ours(args, rank: int, world: int):
         del U, V, sigma
         if not args.no_e2e:
             run_e2e()
+        _rank_info(world)
         return
 
     # ---- accuracy and whole-solve parity (outside the timed region) ----
@@ -563,8 +564,26 @@ def run_ours(args, rank: int, world: int):
         "e2e": e2e, "roofline": roofline, "fp64_roofline": fp64, "cpu_baseline": cpu,
         "clocks": clocks, "gpu_launches": launches,
         "per_step_s": times,
+        "ranks": _rank_info(world),
     }
     print(json.dumps(line), flush=True)
+
+
+def _rank_info(world: int) -> dict:
+    """Process-group evidence: world size, backend, NCCL version, the GPUs
+    the ranks ran on (all-gathered)."""
+    import torch
+
+    info = {"world": world, "device": torch.cuda.get_device_name()}
+    if world > 1:
+        import torch.distributed as dist
+
+        names = [None] * world
+        dist.all_gather_object(names, (dist.get_rank(), torch.cuda.current_device(),
+                                       torch.cuda.get_device_name()))
+        info.update(backend=dist.get_backend(), ranks=names,
+                    nccl=".".join(map(str, torch.cuda.nccl.version())))
+    return info
 
 
 def main():

@@ -104,7 +104,7 @@ def test_tables_without_the_structure_are_rejected():
 
 
 @pytest.mark.parametrize("g,n,w,nplus", [(2, 128, 8, 128), (4, 128, 8, 128), (4, 128, 8, 61),
-                                         (8, 128, 4, 64)])
+                                         (8, 128, 8, 64)])
 def test_sim_workers_bitwise_vs_single_solve_cpu(g, n, w, nplus):
     cfg = J.SolverConfig(block_width=w)
     a = _problem(n, g * n + nplus)
