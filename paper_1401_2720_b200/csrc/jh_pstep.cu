@@ -521,13 +521,17 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
   static std::atomic<int64_t> epoch_ctr{0};
   int64_t epoch = 0;
   if (pdl) cudaMemsetAsync(done, 0xff, sizeof(int64_t) * (2 * ntask + 1), st);
-  // Grams of p-step s+1 in the update launch of p-step s: on for G of at
-  // most 2^26 entries (n = 8192: 0.626 vs 0.649 ms per p-step), off above
-  // (16384^2: 1.86 vs 1.83 ms per p-step)
-#ifndef JH_GMIX_LOG2
-#define JH_GMIX_LOG2 26
-#endif
-  const bool gmix = m * n <= (int64_t(1) << JH_GMIX_LOG2) && w == 32 && nsteps > 1;
+  // Grams of p-step s+1 in the update launch of p-step s (trailing CTAs
+  // that start when their block-columns are final): a gain where the Gram
+  // chains are short (m <= 8192 and G of at most 2^26 entries: n = 8192,
+  // 0.626 vs 0.649 ms per p-step) or where 1-2 tasks per SM leave room for
+  // them (256 tasks at m = 16384: 1.00 vs 1.04 ms); a loss at 512 tasks
+  // (16384^2: 1.83 vs 1.80) and with fewer tasks than SMs, where the split
+  // Gram kernel is faster (profiles/r02/README.md)
+  const int sms = sm_count();
+  const bool gmix = w == 32 && nsteps > 1 &&
+                    ((m <= 8192 && m * n <= (int64_t(1) << 26)) ||
+                     (ntask > sms && ntask <= 2 * sms && m <= 16384));
   if (gmix) {
     cudaMemsetAsync(gcnt, 0, sizeof(int64_t) * ntask, st);
     launch_colpos(outer + (int64_t)first_step * ntask * 2, nsteps, ntask, b, colpos, st);

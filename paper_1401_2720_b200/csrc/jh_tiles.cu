@@ -30,15 +30,52 @@ namespace jh {
 // LDS.64 each) and issues one DMMA per tile: fragment X serves as the A
 // operand (A^T rows) and the B operand alike.
 
-template <int W, int NW, int kGramRch, int kGramStages>
+// Consumer warp cw of CTA part `part` (of SPLIT CTAs per task) acts as warp
+// vw = cw + NW * part of NW * SPLIT virtual warps: it owns the tiles
+// i == vw (mod NW * SPLIT).  SPLIT > 1 spreads one task's tile chains over
+// several SMs (few tasks per p-step: the sharded solve), each CTA streaming
+// the whole pair (the second read of a chunk is an L2 hit).
+template <int W, int VW, int RCH>
+__device__ __forceinline__ void gram_chunk_dispatch(int vw, const double *buf, int nr,
+                                                    double (&acc)[GramTiles<W, VW>::MY][2],
+                                                    int t) {
+  switch (vw) {
+#define JH_GC(k) \
+  case k:        \
+    if constexpr (k < VW) gram_chunk<W, VW, (k < VW ? k : 0), RCH>(buf, nr, acc, t); \
+    break;
+    JH_GC(0) JH_GC(1) JH_GC(2) JH_GC(3) JH_GC(4) JH_GC(5) JH_GC(6) JH_GC(7) JH_GC(8) JH_GC(9)
+#undef JH_GC
+    default: break;
+  }
+}
+
+template <int W, int VW>
+__device__ __forceinline__ void gram_store_dispatch(int vw, double *H,
+                                                    const double (&acc)[GramTiles<W, VW>::MY][2],
+                                                    int g, int t) {
+  switch (vw) {
+#define JH_GS(k) \
+  case k:        \
+    if constexpr (k < VW) gram_store<W, VW, (k < VW ? k : 0)>(H, acc, g, t); \
+    break;
+    JH_GS(0) JH_GS(1) JH_GS(2) JH_GS(3) JH_GS(4) JH_GS(5) JH_GS(6) JH_GS(7) JH_GS(8) JH_GS(9)
+#undef JH_GS
+    default: break;
+  }
+}
+
+template <int W, int NW, int kGramRch, int kGramStages, int SPLIT = 1>
 __global__ void __launch_bounds__(32 * (NW + 1))
 k_gram_tma(const double *__restrict__ G, int64_t ldg, int64_t m,
            const int32_t *__restrict__ pairs, double *__restrict__ Hbuf) {
   // warp 0 produces (TMA bulk copies), warps 1..NW consume (DMMA)
-  constexpr int BW = W / 2, MY = GramTiles<W, NW>::MY, kGramLd = kGramRch + 4;
+  constexpr int BW = W / 2, VW = NW * SPLIT, MY = GramTiles<W, VW>::MY, kGramLd = kGramRch + 4;
+  static_assert(VW <= 10, "at most one virtual warp per tile of w = 32");
   extern __shared__ __align__(128) double sm[];  // [kGramStages][W][kGramLd]
   __shared__ __align__(8) uint64_t full[kGramStages], empty[kGramStages];
-  const int task = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int task = blockIdx.x / SPLIT, part = blockIdx.x % SPLIT;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int p = pairs[2 * task], q = pairs[2 * task + 1];
   const int64_t nchunk = cdiv(m, kGramRch);
@@ -65,7 +102,7 @@ k_gram_tma(const double *__restrict__ G, int64_t ldg, int64_t m,
     }
     return;
   }
-  const int cw = warp - 1;
+  const int vw = (warp - 1) + NW * part;
   double acc[MY][2];
 #pragma unroll
   for (int i = 0; i < MY; i++) acc[i][0] = acc[i][1] = 0.0;
@@ -75,26 +112,12 @@ k_gram_tma(const double *__restrict__ G, int64_t ldg, int64_t m,
     mbar_wait(&full[s], (uint32_t)((c / kGramStages) & 1));
     const double *buf = sm + (size_t)s * W * kGramLd + (size_t)g * kGramLd + t;
     const int nr = (int)min64(kGramRch, m - c * kGramRch);
-    if (cw == 0)
-      gram_chunk<W, NW, 0, kGramRch>(buf, nr, acc, t);
-    else if (NW > 1 && cw == 1)
-      gram_chunk<W, NW, (NW > 1 ? 1 : 0), kGramRch>(buf, nr, acc, t);
-    else if (NW > 2 && cw == 2)
-      gram_chunk<W, NW, (NW > 2 ? 2 : 0), kGramRch>(buf, nr, acc, t);
-    else if (NW > 3 && cw == 3)
-      gram_chunk<W, NW, (NW > 3 ? 3 : 0), kGramRch>(buf, nr, acc, t);
+    gram_chunk_dispatch<W, VW, kGramRch>(vw, buf, nr, acc, t);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
   double *H = Hbuf + (size_t)task * W * W;  // column-major: H[y * W + x] = h[x][y]
-  if (cw == 0)
-    gram_store<W, NW, 0>(H, acc, g, t);
-  else if (NW > 1 && cw == 1)
-    gram_store<W, NW, (NW > 1 ? 1 : 0)>(H, acc, g, t);
-  else if (NW > 2 && cw == 2)
-    gram_store<W, NW, (NW > 2 ? 2 : 0)>(H, acc, g, t);
-  else if (NW > 3 && cw == 3)
-    gram_store<W, NW, (NW > 3 ? 3 : 0)>(H, acc, g, t);
+  gram_store_dispatch<W, VW>(vw, H, acc, g, t);
 }
 
 // ---------------------------------------------------------------------------
@@ -207,12 +230,13 @@ bool gram_tma_ok(int w, int64_t m, int64_t ldg) {
 // consumer warps per Gram CTA: 2 (tiles 5 + 5 for w = 32), or 4 when few
 // tasks meet long columns (tall factors: one CTA per task leaves SMs short
 // of DMMA warps while every tile is a chain over all m rows)
-template <int W, int NW, int RCH, int STG>
+template <int W, int NW, int RCH, int STG, int SPLIT = 1>
 static void launch_gram_nw(const double *G, int64_t ldg, int64_t m, const int32_t *pairs,
                            int ntask, double *Hbuf, cudaStream_t st) {
   const size_t smem = sizeof(double) * (size_t)STG * W * (RCH + 4);
-  ensure_smem((const void *)k_gram_tma<W, NW, RCH, STG>, (int)smem);
-  k_gram_tma<W, NW, RCH, STG><<<ntask, 32 * (NW + 1), smem, st>>>(G, ldg, m, pairs, Hbuf);
+  ensure_smem((const void *)k_gram_tma<W, NW, RCH, STG, SPLIT>, (int)smem);
+  k_gram_tma<W, NW, RCH, STG, SPLIT><<<ntask * SPLIT, 32 * (NW + 1), smem, st>>>(G, ldg, m,
+                                                                               pairs, Hbuf);
 }
 
 // Ring shape by the CTAs an SM must hold for one wave: longer chunks (one
@@ -235,7 +259,28 @@ static void launch_gram_shape(const double *G, int64_t ldg, int64_t m, const int
 template <int W>
 static void launch_gram_t(const double *G, int64_t ldg, int64_t m, const int32_t *pairs,
                           int ntask, double *Hbuf, cudaStream_t st) {
+  // Few tasks per p-step (the sharded solve) leave the Gram latency-bound:
+  // every tile is one chain over all m rows.  Up to half an SM per task, two
+  // CTAs of 5 consumer warps split a task's 10 tiles (one chain per warp);
+  // up to one SM per task, one CTA of 10 (profiles/r02/README.md: Gram per
+  // p-step at 64 tasks 0.187 -> 0.118 ms, at 128 tasks 0.188 -> 0.144 ms).
+#ifndef JH_GS2_DIV
+#define JH_GS2_DIV 2
+#endif
+#ifndef JH_G10_MUL
+#define JH_G10_MUL 1
+#endif
   const int sms = sm_count();
+  if constexpr (W == 32) {
+    if (ntask <= sms / JH_GS2_DIV) {
+      launch_gram_nw<W, 5, 192, 2, 2>(G, ldg, m, pairs, ntask, Hbuf, st);
+      return;
+    }
+    if (ntask <= sms * JH_G10_MUL) {
+      launch_gram_nw<W, 10, 192, 2, 1>(G, ldg, m, pairs, ntask, Hbuf, st);
+      return;
+    }
+  }
   if (ntask < 3 * sms)
     launch_gram_shape<W, 4>(G, ldg, m, pairs, ntask, sms, Hbuf, st);
   else
