@@ -1,5 +1,6 @@
 """Per-sweep time and kernel-class split of the bench.py config 3 solve
-(dev tool):  python tools/sweep_profile.py [n]"""
+(dev tool):  [OVERLAP=1] python tools/sweep_profile.py [n]
+(with OVERLAP=1 the class split is not meaningful: inner includes the update)"""
 
 import ctypes
 import json
@@ -28,11 +29,12 @@ def main():
     solver = Solver(n, J.SolverConfig(), J.Signature(n, n_plus))
     eng = solver.engine
     lib = _lib.load_library()
-    lib.jh_set_overlap(0)  # kernels apart, so the classes separate
-    G = G0.clone()
-    V = torch.eye(n, dtype=torch.float64, device="cuda")
     import os
 
+    overlap = int(os.environ.get("OVERLAP", "0"))
+    lib.jh_set_overlap(overlap)  # 0: kernels apart, so the classes separate
+    G = G0.clone()
+    V = torch.eye(n, dtype=torch.float64, device="cuda")
     nsw = int(os.environ.get("SWEEPS", "30"))
     for sweep in range(nsw):
         lib.jh_profile_begin(4 * eng.nsteps + 16)
@@ -46,7 +48,7 @@ def main():
         lib.jh_profile_end(ms, cnt)
         print(json.dumps({"sweep": sweep + 1, "ms": e0.elapsed_time(e1), "rot": rot,
                           "proper": proper, "tasks_rotated": eng.tasks_rotated[-1],
-                          "gram_ms": ms[0], "inner_ms": ms[1], "update_ms": ms[2] + ms[3]}), flush=True)
+                          "gram_ms": ms[0], "inner_ms": ms[1], "update_ms": ms[2] + ms[3], "overlap": overlap}), flush=True)
         if proper == 0:
             break
 
