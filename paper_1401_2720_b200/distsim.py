@@ -328,11 +328,16 @@ class _Comm:
     """Exchange / reduction backend: torch.distributed (one worker per rank)
     or an in-process simulation (all workers in this process)."""
 
-    def __init__(self, g: int, backend: Optional[str]):
+    def __init__(self, g: int, backend: Optional[str], process_group=None):
         import torch.distributed as dist
 
+        if process_group is not None:
+            # a torch.distributed-compatible object for this rank (e.g. ranks
+            # run as threads of one process, tests/comm_threads.py)
+            dist = process_group
         self.dist = dist
-        self.sim = backend == "sim" or not (dist.is_available() and dist.is_initialized())
+        self.sim = process_group is None and (
+            backend == "sim" or not (dist.is_available() and dist.is_initialized()))
         if not self.sim:
             if dist.get_world_size() != g:
                 raise ValueError(f"process group has {dist.get_world_size()} ranks, need g = {g}")
@@ -348,7 +353,7 @@ def run_distributed(g_matrix, signature: Optional[Signature], g: int,
                     cfg: SolverConfig = SolverConfig(), hybrid_early_stop: bool = False,
                     collect_trace: bool = False, *, backend: Optional[str] = None,
                     engine=None, mapping: Optional[ColumnMapping] = None,
-                    allow_tall: bool = False):
+                    allow_tall: bool = False, process_group=None):
     """Blocked Jacobi (H)SVD over g workers (distsim.py:216-424).
 
     Under an initialised torch.distributed group of world size g each rank
@@ -374,7 +379,7 @@ def run_distributed(g_matrix, signature: Optional[Signature], g: int,
         signature = Signature(n, n)
     if g < 1:
         raise ValueError("need at least one worker")
-    comm = _Comm(g, backend)
+    comm = _Comm(g, backend, process_group)
     if g == 1:
         return block_jacobi(g_matrix, signature, cfg, allow_tall=allow_tall), []
     if n % (2 * g):

@@ -214,11 +214,16 @@ class CudaShardEngine:
 
 
 class _Comm:
-    def __init__(self, g: int, backend: Optional[str]):
+    def __init__(self, g: int, backend: Optional[str], process_group=None):
         import torch.distributed as dist
 
+        if process_group is not None:
+            # a torch.distributed-compatible object for this rank (e.g. ranks
+            # run as threads of one process, tests/comm_threads.py)
+            dist = process_group
         self.dist = dist
-        self.sim = backend == "sim" or not (dist.is_available() and dist.is_initialized())
+        self.sim = process_group is None and (
+            backend == "sim" or not (dist.is_available() and dist.is_initialized()))
         if not self.sim and dist.get_world_size() != g:
             raise ValueError(f"process group has {dist.get_world_size()} ranks, need g = {g}")
         self.rank = None if self.sim else dist.get_rank()
@@ -312,12 +317,14 @@ def _exchange(comm: _Comm, plan: ShardPlan, cfg_from: int, cfg_to: int, locs: di
 def block_jacobi_sharded(g_matrix, signature: Optional[Signature], g: int,
                          cfg: SolverConfig = SolverConfig(), *, backend: Optional[str] = None,
                          engine=None, timer: Optional[Callable] = None,
-                         allow_tall: bool = False) -> HsvdResult:
+                         allow_tall: bool = False, process_group=None) -> HsvdResult:
     """``block_jacobi`` with the block-columns sharded over g workers (one
     per rank of the initialised torch.distributed group, or simulated in
     this process); bitwise equal to ``block_jacobi`` for every g.  Every rank
     passes the same full factor and receives the full result.  ``timer``
-    (sim mode) is called as timer(worker, segment_index, start|stop)."""
+    (sim mode) is called as timer(worker, segment_index, start|stop).
+    ``process_group``: a torch.distributed-compatible object to use instead
+    of the global process group (one per rank)."""
     import torch
 
     from . import _dev
@@ -337,7 +344,7 @@ def block_jacobi_sharded(g_matrix, signature: Optional[Signature], g: int,
     if cfg.solve_v or cfg.shortening != "cholesky":
         raise NotImplementedError("the sharded solve supports Cholesky shortening with V "
                                   "accumulated or not (solve_v: use block_jacobi)")
-    comm = _Comm(g, backend)
+    comm = _Comm(g, backend, process_group)
     if g == 1 and engine is None and comm.sim:
         return block_jacobi(g_matrix, signature, cfg, allow_tall=allow_tall)
     bw = w // 2

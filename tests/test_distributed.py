@@ -196,3 +196,53 @@ def test_gpu_simulated_workers_bitwise_vs_reference(name, dist_golden):
     assert _sha(res.sigma) == m["sigma_sha256"]
     if m["accumulate_v"]:
         assert np.array_equal(res.v, arrs[f"{name}_v"])
+
+
+# ---------------------------------------------------------------------------
+# the per-rank (non-simulated) path with ranks as threads (tests/comm_threads.py)
+
+
+@pytest.mark.parametrize("name", ["g2_bo", "g2_fb"])
+def test_thread_ranks_bitwise_vs_reference_cpu(name, dist_golden):
+    from tests.comm_threads import run_ranks
+
+    meta, arrs = dist_golden
+    m = meta[name]
+    g = arrs["dist_in"]
+    n = g.shape[0]
+    nplus = int((arrs["dist_lambda"] > 0).sum())
+    cfg = _cfg(m)
+    res = run_ranks(m["g"], lambda i, pg: D.run_distributed(
+        g, J.Signature(n, nplus), m["g"], cfg, engine=OracleEngine(n, n, n // m["g"], cfg),
+        process_group=pg)[0], backend="gloo")
+    for r in res:
+        assert [list(s) for s in r.stats] == m["stats"]
+        assert _sha(r.sigma) == m["sigma_sha256"]
+        assert np.array_equal(r.v, arrs[f"{name}_v"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["g2_bo", "g4_fb", "g2_bo_nov"])
+def test_gpu_thread_ranks_device_exchange_vs_reference(name, dist_golden):
+    """run_distributed's per-rank path (device send/receive of the block
+    pairs, all-reduces, all-gather) with CUDA tensors, g ranks as threads on
+    cuda:0, bitwise against the reference goldens."""
+    from tests.comm_threads import run_ranks
+
+    meta, arrs = dist_golden
+    m = meta[name]
+    g = arrs["dist_in"]
+    n = g.shape[0]
+    nplus = int((arrs["dist_lambda"] > 0).sum())
+    cfg = _cfg(m)
+
+    def rank(i, pg):
+        r, _ = D.run_distributed(g, J.Signature(n, nplus), m["g"], cfg, process_group=pg)
+        torch.cuda.synchronize()
+        return r
+
+    for r in run_ranks(m["g"], rank, backend="nccl"):
+        assert [list(s) for s in r.stats] == m["stats"]
+        assert _sha(r.sigma) == m["sigma_sha256"]
+        if m["accumulate_v"]:
+            assert np.array_equal(r.v, arrs[f"{name}_v"])

@@ -176,3 +176,55 @@ def test_gpu_sim_workers_bitwise_vs_block_jacobi(g, n, m, nplus, variant):
     assert np.array_equal(res.sigma, ref.sigma)
     assert np.array_equal(res.u, ref.u)
     assert np.array_equal(res.v, ref.v)
+
+
+# ---------------------------------------------------------------------------
+# the non-simulated (per-rank) path with ranks as threads (tests/comm_threads.py)
+
+
+@pytest.mark.parametrize("g,nplus", [(2, 128), (4, 61)])
+def test_thread_ranks_bitwise_vs_single_solve_cpu(g, nplus):
+    from tests.comm_threads import run_ranks
+
+    n, cfg = 128, J.SolverConfig(block_width=8)
+    a = _problem(n, 7 * g + nplus)
+    ref = _oracle_solve(a, nplus, cfg)
+    res = run_ranks(g, lambda i, pg: SH.block_jacobi_sharded(
+        a, J.Signature(n, nplus), g, cfg, engine=OracleShardEngine(cfg, nplus),
+        process_group=pg), backend="gloo")
+    for r in res:
+        assert r.stats == ref.stats
+        assert np.array_equal(r.sigma, ref.sigma)
+        assert np.array_equal(r.v, ref.v)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("g,n,nplus", [(2, 1024, 1024), (4, 1024, 600), (8, 2048, 2048)])
+def test_gpu_thread_ranks_device_exchange_bitwise(g, n, nplus):
+    """The per-rank path of an NCCL job (send/receive of CUDA super-columns
+    into the staging buffers, counter all-reduces, the final all-gather)
+    with g ranks as threads on cuda:0: bitwise block_jacobi."""
+    from tests.comm_threads import run_ranks
+
+    cfg = J.SolverConfig(block_width=32)
+    rng = np.random.default_rng(n + g)
+    a = rng.standard_normal((n, n))
+    a /= np.linalg.norm(a, axis=0)
+    a = np.asfortranarray(a * np.logspace(0, -5, n))
+    ref = J.block_jacobi(a, J.Signature(n, nplus), cfg)
+    A = torch.from_numpy(a).cuda()
+
+    def rank(i, pg):
+        r = SH.block_jacobi_sharded(A, J.Signature(n, nplus), g, cfg, process_group=pg)
+        torch.cuda.synchronize()
+        return r
+
+    def np_(x):
+        return x.cpu().numpy() if isinstance(x, torch.Tensor) else x
+
+    res = run_ranks(g, rank, backend="nccl")
+    for r in res:
+        assert r.stats == ref.stats
+        assert np.array_equal(np_(r.sigma), ref.sigma)
+        assert np.array_equal(np_(r.u), ref.u)
+        assert np.array_equal(np_(r.v), ref.v)
