@@ -147,7 +147,8 @@ class ClockSampler:
             if len(parts) < 8:
                 continue
             try:
-                rows.append((float(parts[0]), float(parts[1]), float(parts[2]), parts[4:8]))
+                pw = float(parts[3]) if parts[3] not in ("", "[N/A]") else None
+                rows.append((float(parts[0]), float(parts[1]), float(parts[2]), parts[4:8], pw))
             except ValueError:
                 continue
         os.unlink(self.file.name)
@@ -157,9 +158,24 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in loaded for i, v in enumerate(r[3])
                           if v.lower() == "active"})
+        pws = [r[4] for r in loaded if r[4] is not None]
         return {"sm_mhz": statistics.median(r[0] for r in loaded),
                 "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons,
-                "samples": len(rows), "samples_under_load": len(loaded)}
+                "samples": len(rows), "samples_under_load": len(loaded),
+                # the solve runs at the board power limit: energy, not the
+                # clock-peak rooflines, sets its speed (profiles/r02/energy_probe.json)
+                "power_w": statistics.median(pws) if pws else None,
+                "power_limit_w": _power_limit(self.index)}
+
+
+def _power_limit(index: int):
+    try:
+        out = subprocess.run(["nvidia-smi", "-i", str(index), "--query-gpu=enforced.power.limit",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=10).stdout.strip()
+        return float(out)
+    except Exception:
+        return None
 
 
 # ---------------------------------------------------------------------------

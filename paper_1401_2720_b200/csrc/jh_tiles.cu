@@ -134,7 +134,7 @@ constexpr int kUpdWarps = 8;
 constexpr int kUpdRpw = 256;  // rows per warp
 
 template <int W>
-__global__ void __launch_bounds__(32 * kUpdWarps, 1)
+__global__ void __launch_bounds__(32 * kUpdWarps, W == 64 ? 2 : 1)
 k_update_dmma(double *__restrict__ G, int64_t ldg, int64_t m, double *__restrict__ V,
               int64_t ldv, int64_t nv, const int32_t *__restrict__ pairs,
               const double *__restrict__ Vbuf, const int64_t *__restrict__ trot, int nslab_g) {
@@ -196,6 +196,61 @@ k_update_dmma(double *__restrict__ G, int64_t ldg, int64_t m, double *__restrict
         for (int j = 0; j < 2; j++) st_f64(aout(Y, j) + row, acc[Y][j]);
     }
   };
+  if constexpr (W == 64) {
+    // (B fragments re-read from shared memory per use: kept loop-invariant,
+    // all 128 of them would not fit in registers)
+    auto lds_f64 = [](const double *a) {
+      double v;
+      asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(smem_u32(a)));
+      return v;
+    };
+    // 16 A fragments per 8-row block; the 8 output tiles in two halves of
+    // 4 accumulators; column addresses formed on the fly (no per-column
+    // pointer registers); latency hidden by the 16 warps per SM -- no spills
+    const double *pb = A + (int64_t)p * BW * ld, *qb = A + (int64_t)q * BW * ld;
+    // the stride is re-read through an opaque move per use, so the compiler
+    // does not hoist 64 per-column pointers out of the row loop (spills)
+    auto col = [&](int c) -> double * {
+      int64_t l;
+      asm volatile("mov.b64 %0, %1;" : "=l"(l) : "l"(ld));
+      return const_cast<double *>(c < BW ? pb + (int64_t)c * l : qb + (int64_t)(c - BW) * l);
+    };
+    auto load64 = [&](int64_t r0, double (&f)[NK]) {
+      const int64_t row = r0 + g;
+      const bool ok = row < r_end;
+#pragma unroll
+      for (int kk = 0; kk < NK; kk++) f[kk] = ok ? __ldcs(col(4 * kk + t) + row) : 0.0;
+    };
+    auto half = [&](int64_t r0, const double (&f)[NK], int y0) {
+      double acc[4][2];
+#pragma unroll
+      for (int Y = 0; Y < 4; Y++) acc[Y][0] = acc[Y][1] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < NK; kk++) {
+        double b[4];
+#pragma unroll
+        for (int Y = 0; Y < 4; Y++) b[Y] = lds_f64(&vfrag[(kk * NT + y0 + Y) * 32 + lane]);
+#pragma unroll
+        for (int Y = 0; Y < 4; Y++)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(acc[Y][0]), "+d"(acc[Y][1]) : "d"(f[kk]), "d"(b[Y]));
+      }
+      const int64_t row = r0 + g;
+      if (row < r_end) {
+#pragma unroll
+        for (int Y = 0; Y < 4; Y++)
+#pragma unroll
+          for (int j = 0; j < 2; j++) st_f64(col(8 * (y0 + Y) + 2 * t + j) + row, acc[Y][j]);
+      }
+    };
+    double fa[NK];
+#pragma unroll 1
+    for (int64_t r0 = r_begin; r0 < r_end; r0 += 8) {
+      load64(r0, fa);
+#pragma unroll 1
+      for (int h = 0; h < 2; h++) half(r0, fa, 4 * h);
+    }
+  } else {
   double f0[NK], f1[NK], f2[NK];
   load_block(r_begin, f0);
   load_block(r_begin + 8, f1);
@@ -208,6 +263,7 @@ k_update_dmma(double *__restrict__ G, int64_t ldg, int64_t m, double *__restrict
     if (r0 + 16 >= r_end) break;
     load_block(r0 + 32, f1);
     compute_store(r0 + 16, f2);
+  }
   }
 }
 
@@ -224,7 +280,7 @@ k_update_dmma(double *__restrict__ G, int64_t ldg, int64_t m, double *__restrict
 // host launchers
 
 bool gram_tma_ok(int w, int64_t m, int64_t ldg) {
-  return (w == 16 || w == 32) && m % 2 == 0 && ldg % 2 == 0;
+  return (w == 16 || w == 32 || w == 64) && m % 2 == 0 && ldg % 2 == 0;
 }
 
 // consumer warps per Gram CTA: 2 (tiles 5 + 5 for w = 32), or 4 when few
@@ -291,11 +347,13 @@ void launch_gram_tma(const double *G, int64_t ldg, int64_t m, const int32_t *pai
                      int w, double *Hbuf, cudaStream_t st) {
   if (w == 16)
     launch_gram_t<16>(G, ldg, m, pairs, ntask, Hbuf, st);
-  else
+  else if (w == 32)
     launch_gram_t<32>(G, ldg, m, pairs, ntask, Hbuf, st);
+  else  // w = 64: 36 lower tiles over 4 consumer warps (9 chains each), 3 x 64-row ring (104 KB)
+    launch_gram_nw<64, 4, 64, 3>(G, ldg, m, pairs, ntask, Hbuf, st);
 }
 
-bool update_dmma_ok(int w) { return w == 16 || w == 32; }
+bool update_dmma_ok(int w) { return w == 16 || w == 32 || w == 64; }
 
 template <int W>
 static void launch_update_tma_t(double *G, int64_t ldg, int64_t m, double *V, int64_t ldv,
@@ -314,7 +372,9 @@ void launch_update_dmma(double *G, int64_t ldg, int64_t m, double *V, int64_t ld
                         const int32_t *pairs, int ntask, int w, const double *Vbuf,
                         const int64_t *trot, cudaStream_t st) {
   // the TMA ring needs 16-byte aligned columns; the LDG variant takes the rest
-  const bool tma = m % 2 == 0 && ldg % 2 == 0 &&
+  // (w = 64: the V' fragments of a warp would not fit in registers -- the LDG
+  // variant keeps them in shared memory)
+  const bool tma = w != 64 && m % 2 == 0 && ldg % 2 == 0 &&
                    (!V || (nv % 2 == 0 && ldv % 2 == 0));
   if (tma) {
     if (w == 16)
@@ -330,8 +390,11 @@ void launch_update_dmma(double *G, int64_t ldg, int64_t m, double *V, int64_t ld
   if (w == 16)
     k_update_dmma<16><<<grid, 32 * kUpdWarps, 0, st>>>(G, ldg, m, V, ldv, nv, pairs, Vbuf, trot,
                                                         nsg);
-  else
+  else if (w == 32)
     k_update_dmma<32><<<grid, 32 * kUpdWarps, 0, st>>>(G, ldg, m, V, ldv, nv, pairs, Vbuf, trot,
+                                                        nsg);
+  else
+    k_update_dmma<64><<<grid, 32 * kUpdWarps, 0, st>>>(G, ldg, m, V, ldv, nv, pairs, Vbuf, trot,
                                                         nsg);
 }
 
