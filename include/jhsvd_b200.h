@@ -102,8 +102,9 @@ int jh_cholesky(double *H, int c, double *R, int *info, void *stream);
  * diagonal) of A (m x c), c even <= 32, m a positive multiple of c. */
 int jh_qr_peeloff(const double *A, int64_t lda, int64_t m, int c, double *R, void *stream);
 
-/* inner_jacobi (blockkernel.py:346-400) on one c x c factor, c even <= 64.
- * R in place, V = accumulated transformation; out (device int64[5]) =
+/* inner_jacobi (blockkernel.py:346-400) on one c x c factor, c even.
+ * R in place, V = accumulated transformation (any even order c: up to 64
+ * in shared memory, larger orders in global memory); out (device int64[5]) =
  * rotations, proper, sweeps, status (0 ok, 2 zero column, 3 hyperbolic
  * domain), 1-based bad column. */
 int jh_inner_jacobi(double *R, double *V, int c, const int32_t *steps, const int8_t *signs,

@@ -136,8 +136,6 @@ def inner_jacobi(r, colmap, signature: Signature, strategy: PStrategy, max_sweep
         raise ValueError("colmap must list one global index per local column")
     if np.any(np.diff(colmap) <= 0):
         raise ValueError("colmap must be strictly increasing (keeps J partitioned)")
-    if c > 64:
-        raise ValueError("inner_jacobi on the GPU supports orders up to 64")
     signs = torch.tensor([signature.sign(int(g)) for g in colmap], dtype=torch.int8,
                          device=rt.device)
     steps = torch.from_numpy(np.array(as_table(strategy))).to(rt.device)

@@ -409,6 +409,144 @@ __global__ void k_inner_single(double *__restrict__ R, double *__restrict__ V, i
   }
 }
 
+// Inner Jacobi of one c x c factor of any even order above kMaxW
+// (blockkernel.py:346-400: the reference takes any even order).  R and V
+// live in global memory (L2-resident) and one CTA of kWideThreads runs the
+// sweeps: warp k handles pairs k, k + 32, ... of every inner p-step with
+// exactly the per-pair arithmetic of cta_inner_jacobi (lane 0 forms the
+// three in-order chains and the rotation, all lanes apply it), one CTA
+// barrier per p-step.  On failure the smallest failing pair of the first
+// failing p-step is reported, as in the reference.
+constexpr int kWideThreads = 1024;
+
+__global__ void __launch_bounds__(kWideThreads)
+k_inner_wide(double *__restrict__ R, double *__restrict__ V, int c,
+             const int32_t *__restrict__ steps, const int8_t *__restrict__ sg, double tol_c,
+             int max_sweeps, int64_t *out, int *__restrict__ fail) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int half = c / 2;
+  __shared__ unsigned long long s_rot, s_proper;
+  __shared__ int s_fail_min;
+  for (int64_t i = threadIdx.x; i < (int64_t)c * c; i += blockDim.x)
+    V[i] = (i % c == i / c) ? 1.0 : 0.0;
+  if (threadIdx.x == 0) s_fail_min = 0x7fffffff;
+  __syncthreads();
+  int64_t rot = 0, proper = 0;
+  int sweeps = 0, status = 0, bad = 0;
+  for (int sw = 0; sw < max_sweeps; sw++) {
+    if (threadIdx.x == 0) s_rot = s_proper = 0;
+    __syncthreads();
+    unsigned long long a_r = 0, b_r = 0;
+    for (int si = 0; si < c - 1 && !status; si++) {
+      for (int pi = warp; pi < half; pi += nw) {
+        const int p = steps[((int64_t)si * half + pi) * 2];
+        const int q = steps[((int64_t)si * half + pi) * 2 + 1];
+        double cs = 1.0, tn = 0.0;
+        int act = 0, hyp = 0;
+        if (lane == 0) {
+          const double *cp = R + (int64_t)p * c, *cq = R + (int64_t)q * c;
+          double hpp = 0.0, hqq = 0.0, hpq = 0.0;
+          for (int i = 0; i < c; i++) {
+            const double gp = cp[i], gq = cq[i];
+            hpp = fma(gp, gp, hpp);
+            hqq = fma(gq, gq, hqq);
+            hpq = fma(gp, gq, hpq);
+          }
+          int st = 0, bd = 0;
+          if (hpp == 0.0) {
+            st = kZeroColumn;
+            bd = p + 1;
+          } else if (hqq == 0.0) {
+            st = kZeroColumn;
+            bd = q + 1;
+          } else if (!(fabs(hpq) < tol_c * sqrt(hpp) * sqrt(hqq))) {
+            hyp = (sg[p] > 0 && sg[q] < 0) ? 1 : 0;
+            const double t = hyp ? -1.0 : 1.0;
+            if (!rotation_core(hpp, hqq, hpq, t, cs, tn)) {
+              st = kHypDomain;
+              bd = p + 1;
+            } else {
+              a_r++;
+              if (cs != 1.0) b_r++;
+              act = 1;
+              if (!hyp) {
+                const double h1 = fma(-tn, hpq, hpp);
+                const double h2 = fma(tn, hpq, hqq);
+                if ((sg[p] > 0 && h1 < h2) || (sg[p] < 0 && h1 > h2)) act = 2;
+              }
+            }
+          }
+          if (st) {
+            act = -1;
+            fail[pi] = (st << 16) | bd;
+            atomicMin(&s_fail_min, pi);
+          }
+        }
+        act = __shfl_sync(0xffffffffu, act, 0);
+        if (act > 0) {
+          cs = __shfl_sync(0xffffffffu, cs, 0);
+          tn = __shfl_sync(0xffffffffu, tn, 0);
+          hyp = __shfl_sync(0xffffffffu, hyp, 0);
+          const double s = hyp ? tn : -tn;
+          const bool scale = cs != 1.0;
+          for (int i = lane; i < c; i += 32) {
+            double *rp = R + (int64_t)p * c + i, *rq = R + (int64_t)q * c + i;
+            double *vp = V + (int64_t)p * c + i, *vq = V + (int64_t)q * c + i;
+            const double gp = *rp, gq = *rq, xp = *vp, xq = *vq;
+            double np = fma(s, gq, gp), nq = fma(tn, gp, gq);
+            double mp = fma(s, xq, xp), mq = fma(tn, xp, xq);
+            if (scale) {
+              np = np * cs;
+              nq = nq * cs;
+              mp = mp * cs;
+              mq = mq * cs;
+            }
+            if (act == 2) {
+              *rp = nq;
+              *rq = np;
+              *vp = mq;
+              *vq = mp;
+            } else {
+              *rp = np;
+              *rq = nq;
+              *vp = mp;
+              *vq = mq;
+            }
+          }
+        }
+      }
+      __syncthreads();
+      if (s_fail_min != 0x7fffffff) {
+        const int f = fail[s_fail_min];
+        status = f >> 16;
+        bad = f & 0xffff;
+      }
+    }
+    if (status) {
+      sweeps = sw;
+      break;
+    }
+    if (lane == 0) {
+      atomicAdd(&s_rot, a_r);
+      atomicAdd(&s_proper, b_r);
+    }
+    __syncthreads();
+    const unsigned long long ta = s_rot, tb = s_proper;
+    __syncthreads();
+    sweeps++;
+    rot += (int64_t)ta;
+    proper += (int64_t)tb;
+    if (ta == 0) break;
+  }
+  if (threadIdx.x == 0) {
+    out[0] = rot;
+    out[1] = proper;
+    out[2] = sweeps;
+    out[3] = status;
+    out[4] = bad;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host side
 
@@ -687,7 +825,20 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
 // inner_jacobi (blockkernel.py:346-400) on one c x c factor, c even <= 64.
 int jh_inner_jacobi(double *R, double *V, int c, const int32_t *steps, const int8_t *signs,
                     double tol_c, int max_sweeps, int64_t *out, void *stream) {
-  if (c < 2 || c % 2 || c > kMaxW) return -1000;
+  if (c < 2 || c % 2 || c > 0x7fff) return -1000;
+  if (c > kMaxW) {
+    // any larger even order: R, V in global memory, one CTA (k_inner_wide);
+    // a scratch int per pair for the failure report
+    int *fail = nullptr;
+    if (cudaMallocAsync((void **)&fail, sizeof(int) * (c / 2), (cudaStream_t)stream) !=
+        cudaSuccess)
+      return -(int)cudaErrorMemoryAllocation;
+    g_launches++;
+    k_inner_wide<<<1, kWideThreads, 0, (cudaStream_t)stream>>>(R, V, c, steps, signs, tol_c,
+                                                               max_sweeps, out, fail);
+    cudaFreeAsync(fail, (cudaStream_t)stream);
+    return finish((cudaStream_t)stream);
+  }
   const size_t smem = sizeof(double) * 2 * (size_t)c * c;
   ensure_smem((const void *)k_inner_single, (int)(sizeof(double) * 2 * kMaxW * kMaxW));
   g_launches++;

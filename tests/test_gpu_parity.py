@@ -228,3 +228,27 @@ def test_kernel_paths_bitwise(simple, overlap, solves_golden):
     finally:
         lib.jh_set_simple_kernels(0)
         lib.jh_set_overlap(1)
+
+
+@pytest.mark.parametrize("c,nplus,kind", [(96, 96, "rrow"), (128, 70, "rrow"), (256, 256, "mm"),
+                                          (66, 40, "mm")])
+def test_inner_jacobi_wide_orders_vs_oracle(oracle, c, nplus, kind):
+    """Orders above 64 (the reference takes any even order): the global-memory
+    kernel, bitwise against the oracle, trig and hyperbolic."""
+    rng = np.random.default_rng(c + nplus)
+    a = rng.standard_normal((2 * c, c)) * np.logspace(0, -3, c)
+    r = np.linalg.qr(a, mode="r")
+    r = np.asfortranarray(np.triu(r))
+    strat = S.make_strategy(kind, c)
+    signs = [1 if j < nplus else -1 for j in range(c)]
+    try:
+        ro, vo, rot, prop, sw = oracle.inner_jacobi(r, signs, S.as_table(strat), 30)
+    except oracle.OracleError as e:  # the same failure on the GPU
+        with pytest.raises((J.JDefinitenessError, J.RankDeficiencyError)):
+            J.inner_jacobi(r, np.arange(1, c + 1), J.Signature(c, nplus), strat, 30)
+        assert e.kind in ("jdef", "rank")
+        return
+    res = J.inner_jacobi(r, np.arange(1, c + 1), J.Signature(c, nplus), strat, 30)
+    assert (res.rotations, res.proper_rotations, res.inner_sweeps) == (rot, prop, sw)
+    assert np.array_equal(res.r_out, ro)
+    assert np.array_equal(res.v_acc, vo)
