@@ -64,11 +64,16 @@ void launch_inner5(const double *Hbuf, double *Vbuf, int64_t *trot, const int32_
 #ifndef JH_INNER8
 #define JH_INNER8 1
 #endif
-  // the register-resident kernel wins when the SMs hold several tasks each
-  // (throughput: 1.80 vs 1.82 ms per p-step at 512 tasks), the shared-memory
-  // one when tasks run nearly alone (latency: 0.186 vs 0.203 ms per inner
-  // launch at 64 tasks; tools/worker_profile.py, profiles/r02/README.md)
-  if (JH_INNER8 && inner8_ok(w) && ntask > 2 * sm_count()) {
+  // the register-resident kernel, with its V' rotations one inner p-step
+  // late (issued under the next rotation's division / square-root chain),
+  // wins at every task count: 512 tasks 1.763 vs 1.783 ms per p-step, worker
+  // of the sharded solve at 256 / 128 / 64 tasks 0.994 / 0.644 / 0.458 vs
+  // 1.006 / 0.648 / 0.465 ms against the shared-memory kernel
+  // (tools/ab_pstep.py, tools/worker_profile.py; profiles/r02/README.md)
+#ifndef JH_INNER8_PER_SM
+#define JH_INNER8_PER_SM 0
+#endif
+  if (JH_INNER8 && inner8_ok(w) && ntask > JH_INNER8_PER_SM * sm_count()) {
     launch_inner8(Hbuf, Vbuf, trot, pairs, ntask, n_plus, inner, inner_limit, tol_c, counters,
                   pstep, st, from_r, done, epoch, gblock);
     return;

@@ -85,6 +85,24 @@ k_factor_inner8(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
   }
   int me = lane;  // the column this lane holds
   int64_t tot_rot = 0, tot_proper = 0;
+  // V' rotations run one inner p-step late: the update of p-step k is issued
+  // beside the rotation parameters of p-step k + 1 (a ~350-cycle dependent
+  // chain of divisions and square roots that leaves the FP64 pipe idle), in
+  // the same order per column.  A lane without a pending update applies
+  // fma(0, o, v) * 1 = v (V' entries are never -0.0), so the block is
+  // unconditional and the scheduler can interleave it.
+  double pc1 = 0.0, pcs = 1.0;
+  int ppartner = lane;
+  auto v_apply = [&]() {
+#pragma unroll
+    for (int i = 0; i < W; i++) {
+      const double o = __shfl_sync(kFull, vc[i], ppartner);
+      vc[i] = fma(pc1, o, vc[i]) * pcs;
+    }
+    pc1 = 0.0;
+    pcs = 1.0;
+    ppartner = lane;
+  };
   if (!status) {
     for (int sw = 0; sw < inner_limit; sw++) {
       int a_r = 0, b_r = 0;
@@ -111,6 +129,7 @@ k_factor_inner8(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
         bool fast_ok;
         bool rot_ok = rotation_core_fast(hpp, hqq, hpq, hyp ? -1.0 : 1.0, cs, tn, sp, sq,
                                          fast_ok);
+        v_apply();  // the previous p-step's V' rotations
         if (!fast_ok) {
           sp = sqrt(hpp);
           sq = sqrt(hqq);
@@ -149,7 +168,6 @@ k_factor_inner8(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
           bad = __shfl_sync(kFull, fb, src);
           break;
         }
-        const unsigned rot_mask = __ballot_sync(kFull, act != 0);
         if (act) {
           // gp' = fma(s, gq, gp) cs, gq' = fma(tn, gp, gq) cs with s = -tn
           // (trig) or tn (hyperbolic); the * cs is skipped when cs == 1
@@ -161,13 +179,9 @@ k_factor_inner8(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
             if (scale) v = v * cs;
             col[i] = v;
           }
-#pragma unroll
-          for (int i = 0; i < W; i++) {
-            const double o = __shfl_sync(rot_mask, vc[i], partner);
-            double v = fma(c1, o, vc[i]);
-            if (scale) v = v * cs;
-            vc[i] = v;
-          }
+          pc1 = c1;  // V' in the next p-step (v_apply)
+          pcs = scale ? cs : 1.0;
+          ppartner = partner;
           if (act == 2) {  // sorting swap: the lanes trade columns
             me = pcol;
             S.lane_of[me] = (uint8_t)lane;
@@ -176,6 +190,7 @@ k_factor_inner8(const double *__restrict__ Hbuf, double *__restrict__ Vbuf,
         __syncwarp();
       }
       if (status) break;
+      v_apply();  // the sweep's last p-step
       const int ta = __reduce_add_sync(kFull, a_r);
       const int tb = __reduce_add_sync(kFull, b_r);
       tot_rot += ta;
