@@ -328,6 +328,28 @@ def _relaunch_under_torchrun(n: int):
 # our arm
 
 
+def _nvml_handle(index: int):
+    try:
+        import pynvml
+
+        pynvml.nvmlInit()
+        return pynvml.nvmlDeviceGetHandleByIndex(index)
+    except Exception:
+        return None
+
+
+def _energy_j(h):
+    """Total energy the GPU drew since driver load (NVML), joules."""
+    if h is None:
+        return None
+    try:
+        import pynvml
+
+        return pynvml.nvmlDeviceGetTotalEnergyConsumption(h) / 1e3
+    except Exception:
+        return None
+
+
 def fp64_peak():
     p = ROOT / "profiles" / "r02" / "dmma_rate.json"
     if p.exists():
@@ -388,6 +410,8 @@ def run_ours(args, rank: int, world: int):
     if sampler:
         sampler.start()
     launches0 = lib.jh_launch_count()
+    nvml = _nvml_handle(torch.cuda.current_device())
+    energy0 = _energy_j(nvml)
     times = []
     res = None
     for _ in range(args.steps):
@@ -399,6 +423,7 @@ def run_ours(args, rank: int, world: int):
         _barrier(world)
         times.append(_reduce(e0.elapsed_time(e1) / 1e3, world, "max"))
     launches = int(_reduce(float(lib.jh_launch_count() - launches0), world, "sum"))
+    energy1 = _energy_j(nvml)
     clocks = sampler.stop() if sampler else None
     value = statistics.mean(times)
     sigma, U, V, stats, converged = res
@@ -471,6 +496,35 @@ def run_ours(args, rank: int, world: int):
                         "(jh_set_overlap(0)); the timed solves overlap the update with the "
                         "inner Jacobi" + ("; rank 0's kernels" if world > 1 else "")),
     }
+
+    # ---- energy roofline: the solve runs at the board power limit, so its
+    # speed is set by joules, not by the clock-peak rooflines.  Per solve:
+    # the measured energy (NVML counter over the timed region) against the
+    # model's floor from this pool's measured unit costs
+    # (profiles/r02/energy_probe.json): DMMA flops x J/flop + algorithmic
+    # HBM bytes x J/byte + idle power x the measured time.
+    energy = None
+    probe = ROOT / "profiles" / "r02" / "energy_probe.json"
+    if energy0 is not None and energy1 is not None and probe.exists():
+        ep = json.loads(probe.read_text())
+        e_meas = (energy1 - energy0) / args.steps
+        solve_bytes = classes["gram"]["bytes_total"] + bytes_update_total
+        e_dmma = solve_flops * ep["dmma"]["pj_per_flop_above_idle"] * 1e-12
+        e_hbm = solve_bytes * ep["hbm"]["pj_per_byte_above_idle"] * 1e-12
+        e_idle = ep["idle_w"] * value
+        floor = e_dmma + e_hbm + e_idle
+        limit = (clocks or {}).get("power_limit_w") or 1000.0
+        energy = {
+            "joules_per_solve": e_meas, "avg_power_w": e_meas / value if value else None,
+            "model_floor_j": floor, "frac": floor / e_meas if e_meas else None,
+            "model_j": {"dmma": e_dmma, "hbm": e_hbm, "idle": e_idle},
+            # the time at which the floor's dynamic energy would run at the limit
+            "time_at_power_limit_s": (e_dmma + e_hbm) / (limit - ep["idle_w"]),
+            "unit_costs": {"pj_per_dmma_flop": ep["dmma"]["pj_per_flop_above_idle"],
+                           "pj_per_hbm_byte": ep["hbm"]["pj_per_byte_above_idle"],
+                           "idle_w": ep["idle_w"], "source": "profiles/r02/energy_probe.json"},
+            "note": "rank-local GPU" if world > 1 else "one GPU",
+        }
 
     def run_e2e():
         """The same solve through the public API from pinned host memory
@@ -577,7 +631,8 @@ def run_ours(args, rank: int, world: int):
         "sweeps": len(stats), "converged": converged, "stats": [list(s) for s in stats],
         "tasks_rotated_per_sweep": rotated_per_sweep,
         "accuracy": accuracy, "parity": parity,
-        "e2e": e2e, "roofline": roofline, "fp64_roofline": fp64, "cpu_baseline": cpu,
+        "e2e": e2e, "roofline": roofline, "fp64_roofline": fp64, "energy_roofline": energy,
+        "cpu_baseline": cpu,
         "clocks": clocks, "gpu_launches": launches,
         "per_step_s": times,
         "ranks": _rank_info(world),

@@ -116,16 +116,38 @@ __device__ __forceinline__ void vp_transform(double *buf, int cb0, int cb1,
                                              const int64_t (&gcol)[4], int64_t r, int nr, int g,
                                              int t) {
   const int sw = (t >> 1) & 1;  // conflict-free 64-bit shared stores
+  // per-call addressing, hoisted out of the row loop: the shared-memory
+  // column offsets of the 8 A fragments, and per output tile the slot column
+  // and the global column pointer (gcol indexed by the tile's block once
+  // here, not per store)
+  int aoff[8];
+#pragma unroll
+  for (int kk = 0; kk < 8; kk++)
+    aoff[kk] = ((kk < 4 ? cb0 + 4 * kk : cb1 + 4 * kk - 16) + t) * kVLd + g;
+  // value jj of tile Y goes to column n = 8 (Y & 1) + 2t + (jj ^ sw); the
+  // jj = 1 column is the jj = 0 one + (1 - 2 sw)
+  int soff[4];
+  double *gp[4];
+  bool kp[4], tg[4];
+  const int dsj = (1 - 2 * sw) * kVLd;
+  const int64_t dgj = (1 - 2 * sw) * ldv;
+#pragma unroll
+  for (int Y = 0; Y < 4; Y++) {
+    const int cbase = Y < 2 ? cb0 : cb1, blk = cbase >> 4;
+    kp[Y] = (keep >> blk) & 1;
+    tg[Y] = (fin >> blk) & 1;
+    const int64_t gc = blk == 0 ? gcol[0] : blk == 1 ? gcol[1] : blk == 2 ? gcol[2] : gcol[3];
+    const int n = 8 * (Y & 1) + 2 * t + sw;
+    soff[Y] = (cbase + n) * kVLd;
+    gp[Y] = V + (gc + n) * ldv + r;
+  }
 #pragma unroll 1
   for (int rb = 0; rb < kVRch / 8; rb += 2) {
     double a[2][8];
 #pragma unroll
     for (int h = 0; h < 2; h++)
 #pragma unroll
-      for (int kk = 0; kk < 8; kk++) {
-        const int col = (kk < 4 ? cb0 + 4 * kk : cb1 + 4 * kk - 16) + t;
-        a[h][kk] = buf[col * kVLd + 8 * (rb + h) + g];
-      }
+      for (int kk = 0; kk < 8; kk++) a[h][kk] = buf[aoff[kk] + 8 * (rb + h)];
     double acc[2][4][2];
 #pragma unroll
     for (int h = 0; h < 2; h++)
@@ -140,17 +162,14 @@ __device__ __forceinline__ void vp_transform(double *buf, int cb0, int cb1,
 #pragma unroll
     for (int h = 0; h < 2; h++) {
       const int row = 8 * (rb + h) + g;
+      const bool in = row < nr;
 #pragma unroll
       for (int Y = 0; Y < 4; Y++) {
-        const int cbase = Y < 2 ? cb0 : cb1, blk = cbase >> 4;
-        const bool kp = (keep >> blk) & 1, to_g = ((fin >> blk) & 1) && row < nr;
 #pragma unroll
         for (int jj = 0; jj < 2; jj++) {
-          const int j = jj ^ sw;
-          const double v = j ? acc[h][Y][1] : acc[h][Y][0];
-          const int n = 8 * (Y & 1) + 2 * t + j;
-          if (kp) buf[(cbase + n) * kVLd + row] = v;
-          if (to_g) st_f64(V + (gcol[blk] + n) * ldv + r + row, v);
+          const double v = sw ? acc[h][Y][jj ^ 1] : acc[h][Y][jj];
+          if (kp[Y]) buf[soff[Y] + jj * dsj + row] = v;
+          if (tg[Y] && in) st_f64(gp[Y] + jj * dgj + row, v);
         }
       }
     }
