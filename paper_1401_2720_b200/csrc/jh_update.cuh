@@ -79,6 +79,10 @@ __device__ __forceinline__ void update_tma_cta(double *__restrict__ G, int64_t l
     mbar_wait(&full[s], (uint32_t)((c / STAGES) & 1));
     const int64_t r0 = s0 + (int64_t)c * RCH;
     const double *buf = ring + (size_t)s * W * LD;
+    // this warp's rows of the chunk start at row0; the row blocks below are
+    // immediate offsets from per-chunk column pointers
+    const int64_t row0 = r0 + cw * (8 * RB) + g;
+    double *cp = pout + row0, *cq = qout + row0;
 #pragma unroll
     for (int rb = 0; rb < RB; rb++) {
       const int rl = cw * (8 * RB) + rb * 8;
@@ -92,15 +96,14 @@ __device__ __forceinline__ void update_tma_cta(double *__restrict__ G, int64_t l
       for (int kk = 0; kk < NK; kk++)
 #pragma unroll
         for (int Y = 0; Y < NT; Y++) dmma(acc[Y][0], acc[Y][1], a[kk], bf[kk][Y]);
-      const int64_t row = r0 + rl + g;
-      if (row < s1) {
+      if (row0 + rb * 8 < s1) {
 #pragma unroll
         for (int Y = 0; Y < NT; Y++)
 #pragma unroll
           for (int j = 0; j < 2; j++) {
-            double *dst = Y < NT / 2 ? pout + (int64_t)(8 * Y + j) * ld
-                                     : qout + (int64_t)(8 * Y + j - BW) * ld;
-            st_f64(dst + row, acc[Y][j]);
+            double *dst = Y < NT / 2 ? cp + (int64_t)(8 * Y + j) * ld
+                                     : cq + (int64_t)(8 * Y + j - BW) * ld;
+            st_f64(dst + rb * 8, acc[Y][j]);
           }
       }
     }

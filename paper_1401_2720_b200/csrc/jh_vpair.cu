@@ -115,17 +115,19 @@ __device__ __forceinline__ void vp_transform(double *buf, int cb0, int cb1,
                                              unsigned fin, double *V, int64_t ldv,
                                              const int64_t (&gcol)[4], int64_t r, int nr, int g,
                                              int t) {
-  const int sw = (t >> 1) & 1;  // conflict-free 64-bit shared stores
+  // Lanes with t >= 2 (sw = 1) store their two values in the opposite order
+  // (conflict-free 64-bit shared stores).  Their V' fragments carry the
+  // tile's columns 4 <-> 5 and 6 <-> 7 swapped (vp_load_bfrag), so the
+  // accumulator acc[j] already holds column 2t + (j ^ sw): no value select.
+  const int sw = (t >> 1) & 1;
   // per-call addressing, hoisted out of the row loop: the shared-memory
-  // column offsets of the 8 A fragments, and per output tile the slot column
-  // and the global column pointer (gcol indexed by the tile's block once
-  // here, not per store)
+  // column offsets of the 8 A fragments, and per output tile and value the
+  // slot column and the global column pointer at row g
   int aoff[8];
 #pragma unroll
   for (int kk = 0; kk < 8; kk++)
     aoff[kk] = ((kk < 4 ? cb0 + 4 * kk : cb1 + 4 * kk - 16) + t) * kVLd + g;
-  // value jj of tile Y goes to column n = 8 (Y & 1) + 2t + (jj ^ sw); the
-  // jj = 1 column is the jj = 0 one + (1 - 2 sw)
+  // (value j = 1 sits in the column of value 0 plus 1 - 2 sw)
   int soff[4];
   double *gp[4];
   bool kp[4], tg[4];
@@ -138,8 +140,8 @@ __device__ __forceinline__ void vp_transform(double *buf, int cb0, int cb1,
     tg[Y] = (fin >> blk) & 1;
     const int64_t gc = blk == 0 ? gcol[0] : blk == 1 ? gcol[1] : blk == 2 ? gcol[2] : gcol[3];
     const int n = 8 * (Y & 1) + 2 * t + sw;
-    soff[Y] = (cbase + n) * kVLd;
-    gp[Y] = V + (gc + n) * ldv + r;
+    soff[Y] = (cbase + n) * kVLd + g;
+    gp[Y] = V + (gc + n) * ldv + r + g;
   }
 #pragma unroll 1
   for (int rb = 0; rb < kVRch / 8; rb += 2) {
@@ -159,28 +161,30 @@ __device__ __forceinline__ void vp_transform(double *buf, int cb0, int cb1,
       for (int h = 0; h < 2; h++)
 #pragma unroll
         for (int Y = 0; Y < 4; Y++) dmma(acc[h][Y][0], acc[h][Y][1], a[h][kk], bf[kk][Y]);
+    const int ro = 8 * rb;
 #pragma unroll
     for (int h = 0; h < 2; h++) {
-      const int row = 8 * (rb + h) + g;
-      const bool in = row < nr;
+      const bool in = ro + 8 * h + g < nr;
 #pragma unroll
       for (int Y = 0; Y < 4; Y++) {
 #pragma unroll
-        for (int jj = 0; jj < 2; jj++) {
-          const double v = sw ? acc[h][Y][jj ^ 1] : acc[h][Y][jj];
-          if (kp[Y]) buf[soff[Y] + jj * dsj + row] = v;
-          if (tg[Y] && in) st_f64(gp[Y] + jj * dgj + row, v);
+        for (int j = 0; j < 2; j++) {
+          if (kp[Y]) buf[soff[Y] + (j ? dsj : 0) + ro + 8 * h] = acc[h][Y][j];
+          if (tg[Y] && in) st_f64(gp[Y] + (j ? dgj : 0) + ro + 8 * h, acc[h][Y][j]);
         }
       }
     }
   }
 }
 
+// B fragments of V' (lane: row 4kk + t, column 8Y + g), with columns
+// 4 <-> 5 and 6 <-> 7 of every 8-column tile swapped (see vp_transform)
 __device__ __forceinline__ void vp_load_bfrag(double (&bf)[8][4], const double *Vt, int g, int t) {
+  const int gs = g >= 4 ? g ^ 1 : g;
 #pragma unroll
   for (int kk = 0; kk < 8; kk++)
 #pragma unroll
-    for (int Y = 0; Y < 4; Y++) bf[kk][Y] = Vt[(8 * Y + g) * kVW + 4 * kk + t];
+    for (int Y = 0; Y < 4; Y++) bf[kk][Y] = Vt[(8 * Y + gs) * kVW + 4 * kk + t];
 }
 
 // one CTA: cycle c, V row slab k
