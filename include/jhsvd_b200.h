@@ -99,7 +99,8 @@ int jh_gram(const double *A, int64_t lda, int64_t m, int c, double *H, void *str
 int jh_cholesky(double *H, int c, double *R, int *info, void *stream);
 
 /* qr_peeloff (blockkernel.py:223-244): R (c x c, column-major, nonnegative
- * diagonal) of A (m x c), c even <= 32, m a positive multiple of c. */
+ * diagonal) of A (m x c), c even <= 256, m a positive multiple of c (widths
+ * above 32 in a global-memory kernel). */
 int jh_qr_peeloff(const double *A, int64_t lda, int64_t m, int c, double *R, void *stream);
 
 /* inner_jacobi (blockkernel.py:346-400) on one c x c factor, c even.

@@ -180,7 +180,7 @@ def qr_peeloff(gpair):
     """Upper-triangular factor of a tall block-column pair by per-chunk
     Householder QRs merged with Givens peel-off stages (blockkernel.py:223-244);
     nonnegative diagonal.  The row count must be a multiple of the column
-    count (even, <= 32 on the GPU)."""
+    count (even, <= 256 on the GPU)."""
     from . import _dev
 
     lib = _lib.require_cuda()
@@ -190,8 +190,8 @@ def qr_peeloff(gpair):
     c, m = (int(x) for x in a.shape)
     if m % c or m < c:
         raise ValueError(f"row count {m} must be a positive multiple of {c}")
-    if c % 2 or c > 32:
-        raise NotImplementedError("qr_peeloff runs on the GPU for even widths up to 32")
+    if c % 2 or c > 256:
+        raise NotImplementedError("qr_peeloff runs on the GPU for even widths up to 256")
     r = torch.empty((c, c), dtype=torch.float64, device=a.device)
     _lib.check(lib.jh_qr_peeloff(a.data_ptr(), m, m, c, r.data_ptr(), _lib.stream_handle()),
                "qr_peeloff")

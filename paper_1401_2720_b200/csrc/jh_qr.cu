@@ -58,7 +58,8 @@ __device__ __forceinline__ double qr_selected(const double *x, int n, double lo,
 // norm2_unscaled (robustnorm.py:303-308) of a vector of n <= 256 entries
 // (one leaf), by one thread: _sum_squares_core (robustnorm.py:242-292) then
 // norm2 (:295-300)
-__device__ double qr_norm2(const double *x, int n, const QrBounds &bd) {
+template <class Bounds>
+__device__ double qr_norm2(const double *x, int n, const Bounds &bd) {
   if (n == 0) return 0.0;
   double big = 0.0, small = kNu;
   for (int i = 0; i < n; i++) {
@@ -271,8 +272,138 @@ k_qr_peeloff(const double *__restrict__ G, int64_t ldg, int64_t m,
   }
 }
 
+// ---- any even width up to kQrWideMax: the same algorithm with the blocks in
+// global memory (L2-resident scratch, one CTA of kQrWideThreads per task):
+// thread j owns column j in the Householder updates, thread x row x of a
+// peel-off stage.  Column norms of up to kQrWideMax - 1 entries are one leaf
+// of the reference's robust norm (robustnorm.py:242-308): qr_norm2 with a
+// bounds table for lengths up to kQrWideMax.
+constexpr int kQrWideMax = 256;
+constexpr int kQrWideThreads = 256;
+
+struct QrBoundsWide {
+  double mu[kQrWideMax + 1], nu[kQrWideMax + 1];
+};
+
+static const QrBoundsWide &qr_bounds_wide() {
+  static const QrBoundsWide b = [] {
+    QrBoundsWide t{};
+    for (int n = 1; n <= kQrWideMax; n++) jh_safe_bounds(n, &t.mu[n], &t.nu[n]);
+    return t;
+  }();
+  return b;
+}
+
+// _householder_qr of a c x c block (column-major, ld c) by the CTA
+__device__ void qr_householder_cta(double *a, int c, const QrBoundsWide &bd, double *sc) {
+  const int tid = threadIdx.x;
+  for (int k = 0; k < c - 1; k++) {
+    if (tid == 0) {
+      const double alpha = a[(int64_t)k * c + k];
+      const double xnorm = qr_norm2(a + (int64_t)k * c + k + 1, c - k - 1, bd);
+      double skip = 1.0, tau = 0.0, denom = 1.0, beta = 0.0;
+      if (xnorm != 0.0) {
+        const double nr = qr_hypot2(alpha, xnorm);
+        beta = alpha >= 0.0 ? -nr : nr;
+        tau = (beta - alpha) / beta;
+        denom = alpha - beta;
+        skip = 0.0;
+      }
+      sc[0] = skip;
+      sc[1] = tau;
+      sc[2] = denom;
+      sc[3] = beta;
+    }
+    __syncthreads();
+    const bool skip = sc[0] != 0.0;
+    const double tau = sc[1], denom = sc[2], beta = sc[3];
+    if (!skip) {
+      for (int i = k + 1 + tid; i < c; i += blockDim.x)
+        a[(int64_t)k * c + i] = a[(int64_t)k * c + i] / denom;
+    }
+    __syncthreads();
+    if (!skip) {
+      if (tid == 0) a[(int64_t)k * c + k] = beta;
+      const double *ck = a + (int64_t)k * c;
+      for (int j = k + 1 + tid; j < c; j += blockDim.x) {
+        double *cj = a + (int64_t)j * c;
+        double z = cj[k];
+        for (int i = k + 1; i < c; i++) z = fma(ck[i], cj[i], z);
+        const double tz = tau * z;
+        cj[k] = cj[k] - tz;
+        for (int i = k + 1; i < c; i++) cj[i] = fma(-tz, ck[i], cj[i]);
+      }
+    }
+    __syncthreads();
+  }
+  for (int j = tid; j < c; j += blockDim.x)
+    for (int i = j + 1; i < c; i++) a[(int64_t)j * c + i] = 0.0;
+  __syncthreads();
+}
+
+// _peel_combine of r1 into r0 (both c x c, ld c) by the CTA
+__device__ void qr_peel_cta(double *r0, double *r1, int c) {
+  for (int k = 0; k < c; k++) {
+    for (int x = k + threadIdx.x; x < c; x += blockDim.x) {
+      const int xr = x - k;
+      const double b = r1[(int64_t)x * c + xr];
+      if (b != 0.0) {
+        double cc, ss;
+        qr_givens(r0[(int64_t)x * c + x], b, cc, ss);
+        for (int j = x; j < c; j++) {
+          const double v0 = r0[(int64_t)j * c + x];
+          const double v1 = r1[(int64_t)j * c + xr];
+          r0[(int64_t)j * c + x] = fma(ss, v1, cc * v0);
+          r1[(int64_t)j * c + xr] = fma(cc, v1, -(ss * v0));
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kQrWideThreads)
+k_qr_wide(const double *__restrict__ G, int64_t ldg, int64_t m, int c,
+          const int32_t *__restrict__ pairs, double *__restrict__ Rbuf, double *__restrict__ scr,
+          const __grid_constant__ QrBoundsWide bd) {
+  __shared__ double sc[4];
+  const int task = blockIdx.x, bw = c / 2;
+  const int64_t p = pairs ? pairs[2 * task] : 0, q = pairs ? pairs[2 * task + 1] : 1;
+  const int64_t cc2 = (int64_t)c * c;
+  double *r0 = Rbuf + (int64_t)task * cc2;   // the running factor, in place in Rbuf
+  double *r1 = scr + (int64_t)task * cc2;
+  const int64_t nchunk = m / c;
+  for (int64_t ch = 0; ch < nchunk; ch++) {
+    double *a = ch == 0 ? r0 : r1;
+    for (int64_t e = threadIdx.x; e < cc2; e += blockDim.x) {
+      const int j = (int)(e / c), i = (int)(e - (int64_t)j * c);
+      const int64_t col = j < bw ? p * bw + j : q * bw + (j - bw);
+      a[e] = G[col * ldg + ch * c + i];
+    }
+    __syncthreads();
+    qr_householder_cta(a, c, bd, sc);
+    if (ch > 0) qr_peel_cta(r0, r1, c);
+  }
+  // nonnegative diagonal
+  for (int i = threadIdx.x; i < c; i += blockDim.x)
+    if (r0[(int64_t)i * c + i] < 0.0)
+      for (int j = i; j < c; j++) r0[(int64_t)j * c + i] = -r0[(int64_t)j * c + i];
+}
+
+static int launch_qr_wide(const double *G, int64_t ldg, int64_t m, const int32_t *pairs,
+                          int ntask, int w, double *Rbuf, cudaStream_t st) {
+  double *scr = nullptr;
+  if (cudaMallocAsync((void **)&scr, sizeof(double) * (size_t)ntask * w * w, st) != cudaSuccess)
+    return -(int)cudaErrorMemoryAllocation;
+  k_qr_wide<<<ntask, kQrWideThreads, 0, st>>>(G, ldg, m, w, pairs, Rbuf, scr, qr_bounds_wide());
+  cudaFreeAsync(scr, st);
+  return 0;
+}
+
 // widths of the GPU QR path (the inner Jacobi that takes R is the v5 kernel)
-bool qr_ok(int w, int64_t m) { return (w == 16 || w == 32) && m % w == 0 && m >= w; }
+bool qr_ok(int w, int64_t m) {
+  return (w == 16 || w == 32 || w == 64) && m % w == 0 && m >= w;
+}
 
 template <int W>
 static void launch_qr_t(const double *G, int64_t ldg, int64_t m, const int32_t *pairs, int ntask,
@@ -291,17 +422,27 @@ void launch_qr_peeloff(const double *G, int64_t ldg, int64_t m, const int32_t *p
     JH_QR_CASE(14) JH_QR_CASE(16) JH_QR_CASE(18) JH_QR_CASE(20) JH_QR_CASE(22)
     JH_QR_CASE(24) JH_QR_CASE(26) JH_QR_CASE(28) JH_QR_CASE(30) JH_QR_CASE(32)
 #undef JH_QR_CASE
-    default: break;
+    default:
+      if (w <= kQrWideMax) launch_qr_wide(G, ldg, m, pairs, ntask, w, Rbuf, st);
+      break;
   }
 }
 
 }  // namespace jh
 
-// qr_peeloff (blockkernel.py:223-244) of one m x c pair (c even <= 32, m a
-// positive multiple of c): R (c x c, column-major, nonnegative diagonal).
+// qr_peeloff (blockkernel.py:223-244) of one m x c pair (c even <= 256, m a
+// positive multiple of c): R (c x c, column-major, nonnegative diagonal);
+// widths above 32 run the global-memory kernel k_qr_wide.
 extern "C" int jh_qr_peeloff(const double *A, int64_t lda, int64_t m, int c, double *R,
                              void *stream) {
-  if (c < 2 || c > jh::kQrMaxW || c % 2 || m < c || m % c) return -1000;
+  if (c < 2 || c > jh::kQrWideMax || c % 2 || m < c || m % c) return -1000;
+  if (c > jh::kQrMaxW) {
+    jh::g_launches++;
+    const int rc = jh::launch_qr_wide(A, lda, m, nullptr, 1, c, R, (cudaStream_t)stream);
+    if (rc) return rc;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : -(int)e;
+  }
   jh::launch_qr_peeloff(A, lda, m, nullptr, 1, c, R, (cudaStream_t)stream);
   jh::g_launches++;
   const cudaError_t e = cudaGetLastError();

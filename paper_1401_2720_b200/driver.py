@@ -121,10 +121,10 @@ class SweepEngine:
         w = cfg.block_width
         if w > MAX_GPU_BLOCK_WIDTH:
             raise ValueError(f"block_width {w} > {MAX_GPU_BLOCK_WIDTH} is not supported on the GPU")
-        if cfg.shortening == "qr" and (w not in (16, 32) or m % w):
+        if cfg.shortening == "qr" and (w not in (16, 32, 64) or m % w):
             raise NotImplementedError(
-                "QR peel-off shortening runs on the GPU for block widths 16 and 32 with "
-                "m a multiple of the width")
+                "QR peel-off shortening runs on the GPU for block widths 16, 32 and 64 "
+                "with m a multiple of the width")
         self.shortening = 1 if cfg.shortening == "qr" else 0
         self.m, self.n, self.nv, self.w = m, n, nv, w
         self.cfg = cfg

@@ -58,7 +58,7 @@ def test_qr_peeloff_bitwise(kernels_golden):
         assert np.array_equal(J.qr_peeloff(K[f"qr{k}_in"]), K[f"qr{k}_out"]), k
 
 
-@pytest.mark.parametrize("n,w,kappa", [(512, 32, 1e8), (256, 16, 1e12)])
+@pytest.mark.parametrize("n,w,kappa", [(512, 32, 1e8), (256, 16, 1e12), (512, 64, 1e6)])
 def test_qr_shortening_bitwise_vs_oracle(n, w, kappa, oracle):
     """The QR peel-off sweep path (SolverConfig.shortening = 'qr') against
     the C oracle on a graded factor, bitwise."""
@@ -252,3 +252,13 @@ def test_inner_jacobi_wide_orders_vs_oracle(oracle, c, nplus, kind):
     assert (res.rotations, res.proper_rotations, res.inner_sweeps) == (rot, prop, sw)
     assert np.array_equal(res.r_out, ro)
     assert np.array_equal(res.v_acc, vo)
+
+
+@pytest.mark.parametrize("m,c,scale", [(192, 48, 1.0), (512, 64, 1e-3), (1024, 128, 1e150),
+                                       (512, 256, 1e-150)])
+def test_qr_peeloff_wide_widths_vs_oracle(oracle, m, c, scale):
+    """Widths above 32 (the reference takes any even width): the global-memory
+    kernel against the oracle, bitwise, including the scaled-norm branches."""
+    rng = np.random.default_rng(m + c)
+    a = np.asfortranarray(rng.standard_normal((m, c)) * np.logspace(0, -4, c) * scale)
+    assert np.array_equal(J.qr_peeloff(a), oracle.qr_peeloff(a))
