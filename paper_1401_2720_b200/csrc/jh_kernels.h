@@ -61,11 +61,6 @@ int64_t cycle_plan_ints(int b, int steps);
 int cycle_plan(const int32_t *outer, int b, int steps, int32_t *plan);
 
 // ---- engine 1 update launches (jh_vpair.cu)
-// V update of the p-step pair (sa, sa+1) (or sa alone), per cycle and row
-// slab, from the tasks' V' and rotation counts
-void launch_vpair(double *V, int64_t ldv, int64_t nv, const int32_t *outer, const int32_t *plan,
-                  int b, int steps, int sa, bool second, const double *VpA, const int64_t *rotA,
-                  const double *VpB, const int64_t *rotB, cudaStream_t st);
 // one launch: the G update of one p-step (pairs / Vbuf / trot as for
 // launch_update_dmma) and V-pair row slabs of up to two sources; with
 // pairs_next the Grams of p-step cur_step + 1 run as trailing CTAs that wait

@@ -58,7 +58,6 @@ constexpr int kVCols = 64;
 constexpr int kVStages = JH_VSTG;    // ring stages of the V items
 constexpr int kVRch = JH_VRCH;       // rows per V-item chunk
 constexpr int kVLd = kVRch + 4;      // = 4 (mod 16): conflict-free 64-bit shared accesses
-constexpr int kVSlab = 512;  // V rows per CTA of the separate V pass (launch_vpair)
 // Row slabs of the mixed launch: from 256 tasks per p-step on, longer G and
 // V slabs (fewer CTAs, less pipeline fill and drain per CTA); below that the
 // short ones keep enough CTAs for the SMs.  A/B at n = 16384 (ms per
@@ -267,11 +266,6 @@ __device__ __forceinline__ void vpair_cta(const VpArgs &a, int c, int k, VpSmem 
     __syncwarp();
     if (lane == 0) mbar_arrive(phaseA ? &S.adone[st] : &S.empty[st]);
   }
-}
-
-__global__ void __launch_bounds__(160, 2) k_vpair(VpArgs a) {
-  extern __shared__ __align__(128) unsigned char smraw[];
-  vpair_cta(a, blockIdx.x, blockIdx.y, *reinterpret_cast<VpSmem *>(smraw));
 }
 
 // ---- Gram of one task of the next p-step inside the update launch -----------------
@@ -493,32 +487,6 @@ __global__ void __launch_bounds__(160, JH_MIX_MINB) k_update_mix(MixArgs a) {
 void launch_colpos(const int32_t *outer, int nsteps, int T, int b, int32_t *colpos,
                    cudaStream_t st) {
   k_colpos<<<256, 256, 0, st>>>(outer, nsteps, T, b, colpos);
-}
-
-void launch_vpair(double *V, int64_t ldv, int64_t nv, const int32_t *outer, const int32_t *plan,
-                  int b, int steps, int sa, bool second, const double *VpA, const int64_t *rotA,
-                  const double *VpB, const int64_t *rotB, cudaStream_t st) {
-  VpArgs a{};
-  a.doneA = a.doneB = nullptr;
-  a.V = V;
-  a.ldv = ldv;
-  a.nv = nv;
-  a.outer = outer;
-  a.cyc = plan;
-  a.S = steps;
-  a.T = b / 2;
-  a.ncyc = a.T / 2;
-  a.sa = sa;
-  a.second = second;
-  a.VpA = VpA;
-  a.VpB = VpB ? VpB : VpA;
-  a.rotA = rotA;
-  a.rotB = rotB ? rotB : rotA;
-  a.vslab = kVSlab;
-  const size_t smem = sizeof(VpSmem);
-  ensure_smem((const void *)k_vpair, (int)smem);
-  dim3 grid(a.ncyc, (unsigned)cdiv(nv, kVSlab));
-  k_vpair<<<grid, 160, smem, st>>>(a);
 }
 
 void launch_update_mix(double *G, int64_t ldg, int64_t m, const int32_t *pairs, int ntask,
