@@ -422,7 +422,8 @@ constexpr int kWideThreads = 1024;
 __global__ void __launch_bounds__(kWideThreads)
 k_inner_wide(double *__restrict__ R, double *__restrict__ V, int c,
              const int32_t *__restrict__ steps, const int8_t *__restrict__ sg, double tol_c,
-             int max_sweeps, int64_t *out, int *__restrict__ fail) {
+             int max_sweeps, int64_t *out) {
+  extern __shared__ int fail[];  // per pair of the current p-step: (status << 16) | column
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int half = c / 2;
   __shared__ unsigned long long s_rot, s_proper;
@@ -828,15 +829,12 @@ int jh_inner_jacobi(double *R, double *V, int c, const int32_t *steps, const int
   if (c < 2 || c % 2 || c > 0x7fff) return -1000;
   if (c > kMaxW) {
     // any larger even order: R, V in global memory, one CTA (k_inner_wide);
-    // a scratch int per pair for the failure report
-    int *fail = nullptr;
-    if (cudaMallocAsync((void **)&fail, sizeof(int) * (c / 2), (cudaStream_t)stream) !=
-        cudaSuccess)
-      return -(int)cudaErrorMemoryAllocation;
+    // one shared int per pair for the failure report
+    const int smem = (int)sizeof(int) * (c / 2);
+    ensure_smem((const void *)k_inner_wide, smem);
     g_launches++;
-    k_inner_wide<<<1, kWideThreads, 0, (cudaStream_t)stream>>>(R, V, c, steps, signs, tol_c,
-                                                               max_sweeps, out, fail);
-    cudaFreeAsync(fail, (cudaStream_t)stream);
+    k_inner_wide<<<1, kWideThreads, smem, (cudaStream_t)stream>>>(R, V, c, steps, signs, tol_c,
+                                                                  max_sweeps, out);
     return finish((cudaStream_t)stream);
   }
   const size_t smem = sizeof(double) * 2 * (size_t)c * c;
