@@ -60,7 +60,9 @@ int jh_cycle_plan(const int32_t *outer, int b, int steps, int32_t *plan);
  * post-multiplication of [Gp Gq] and [Vp Vq] (:407-428).
  *   G      m x n (ld ldg), updated in place;
  *   V      nv x n (ld ldv) or NULL, updated in place;
- *   w      block width (shortened order), even, 2 <= w <= 64, n % w == 0;
+ *   w      block width (shortened order), even, 2 <= w <= 8190, n % w == 0
+ *          (above 64: one task at a time through general-purpose kernels;
+ *          shortening 0 only);
  *   plan   device copy of jh_cycle_plan for `outer` or NULL;
  *   gblock NULL, or device int32[b]: the global block-column index of each
  *          local block-column (sharded solves; the J signature of a column

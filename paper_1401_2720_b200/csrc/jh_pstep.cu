@@ -17,6 +17,7 @@
 // workspace that stays L2-resident.
 #include "jh_common.cuh"
 #include "jh_kernels.h"
+#include "jhsvd_b200.h"
 
 #include <atomic>
 
@@ -422,9 +423,13 @@ constexpr int kWideThreads = 1024;
 __global__ void __launch_bounds__(kWideThreads)
 k_inner_wide(double *__restrict__ R, double *__restrict__ V, int c,
              const int32_t *__restrict__ steps, const int8_t *__restrict__ sg, double tol_c,
-             int max_sweeps, int64_t *out) {
+             int max_sweeps, int64_t *out, const int *skip = nullptr) {
   extern __shared__ int fail[];  // per pair of the current p-step: (status << 16) | column
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (skip && *skip) {  // the factorisation failed (sweep_wide): nothing to do
+    if (threadIdx.x < 5) out[threadIdx.x] = 0;
+    return;
+  }
   const int half = c / 2;
   __shared__ unsigned long long s_rot, s_proper;
   __shared__ int s_fail_min;
@@ -546,6 +551,127 @@ k_inner_wide(double *__restrict__ R, double *__restrict__ V, int c,
     out[3] = status;
     out[4] = bad;
   }
+}
+
+// ---------------------------------------------------------------------------
+// Block widths above kMaxW (the reference takes any even width,
+// driver.py:73-74): each task of a p-step in turn through the
+// general-purpose kernels -- the pair gathered into a contiguous m x w
+// scratch, DMMA SYRK (jh_gram), blocked Cholesky (jh_cholesky), the
+// global-memory inner Jacobi (k_inner_wide), DMMA GEMM (jh_gemm) and the
+// scatter back when the task rotated (driver.py:165) -- every entry in the
+// reference's order, as in the fused kernels.  A correctness path: one task
+// at a time, ~15 launches per task.
+
+__global__ void k_pair_gather(const double *__restrict__ src, int64_t lds, int64_t rows,
+                              const int32_t *__restrict__ pairs, int task, int bw,
+                              double *__restrict__ A) {
+  const int64_t p = pairs[2 * task], q = pairs[2 * task + 1];
+  const int64_t total = rows * 2 * bw;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / rows, i = e - j * rows;
+    const int64_t col = j < bw ? p * bw + j : q * bw + (j - bw);
+    A[e] = src[col * lds + i];
+  }
+}
+
+__global__ void k_pair_scatter(const double *__restrict__ B, int64_t rows, double *__restrict__ dst,
+                               int64_t ldd, const int32_t *__restrict__ pairs, int task, int bw,
+                               const int64_t *__restrict__ trot) {
+  if (trot[task] == 0) return;  // no rotations: the pair stays as it is
+  const int64_t p = pairs[2 * task], q = pairs[2 * task + 1];
+  const int64_t total = rows * 2 * bw;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / rows, i = e - j * rows;
+    const int64_t col = j < bw ? p * bw + j : q * bw + (j - bw);
+    dst[col * ldd + i] = B[e];
+  }
+}
+
+// J signature of the task's local columns (global index + 1 <= n_plus: +1)
+__global__ void k_task_signs(const int32_t *__restrict__ pairs, int task, int bw,
+                             const int32_t *__restrict__ gblock, int64_t n_plus, int8_t *sg) {
+  const int64_t p = pairs[2 * task], q = pairs[2 * task + 1];
+  const int64_t gp = gblock ? gblock[p] : p, gq = gblock ? gblock[q] : q;
+  for (int j = threadIdx.x; j < 2 * bw; j += blockDim.x) {
+    const int64_t gcol = (j < bw ? gp * bw + j : gq * bw + (j - bw)) + 1;
+    sg[j] = gcol <= n_plus ? 1 : -1;
+  }
+}
+
+// the task's outcome: counters, rotation flag, first-error key; the
+// Cholesky status is cleared for the next task
+__global__ void k_task_finish(const int64_t *out, int *info, int pstep, int task, int64_t *trot,
+                              unsigned long long *counters) {
+  if (threadIdx.x != 0) return;
+  if (*info) {
+    trot[task] = 0;
+    atomicMin(&counters[2], err_key(pstep, task, kCholesky, *info));
+    *info = 0;
+    return;
+  }
+  if (out[3]) {
+    trot[task] = 0;
+    atomicMin(&counters[2], err_key(pstep, task, (int)out[3], (int)out[4]));
+    return;
+  }
+  trot[task] = out[0];
+  atomicAdd(&counters[0], (unsigned long long)out[0]);
+  atomicAdd(&counters[1], (unsigned long long)out[1]);
+  if (out[0]) atomicAdd(&counters[3], 1ull);
+}
+
+static int sweep_wide(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int64_t ldv,
+                      int64_t nv, int w, const int32_t *outer, const int32_t *gblock,
+                      int first_step, int nsteps, const int32_t *inner, int64_t n_plus,
+                      int inner_limit, double tol_c, void *workspace,
+                      unsigned long long *counters, cudaStream_t st) {
+  const int bw = w / 2, ntask = (int)(n / w);
+  const int64_t ww = (int64_t)w * w, rows = V && nv > m ? nv : m;
+  int64_t *trot = (int64_t *)workspace;  // per task of the current p-step
+  // scratch: A, B (rows x w), H, R, V' (w x w), out[5], info, signs
+  const size_t bytes = sizeof(double) * (2 * rows * w + 3 * ww) + 8 * 8 + 8 + (size_t)w + 64;
+  char *scr = nullptr;
+  if (cudaMallocAsync((void **)&scr, bytes, st) != cudaSuccess)
+    return -(int)cudaErrorMemoryAllocation;
+  double *A = (double *)scr, *B = A + rows * w, *H = B + rows * w, *R = H + ww, *Vp = R + ww;
+  int64_t *out = (int64_t *)(Vp + ww);
+  int *info = (int *)(out + 8);
+  int8_t *sg = (int8_t *)(info + 2);
+  cudaMemsetAsync(info, 0, sizeof(int), st);
+  const int smem_inner = (int)sizeof(int) * (w / 2);
+  ensure_smem((const void *)k_inner_wide, smem_inner);
+  auto grid_for = [](int64_t total) { return (unsigned)min64(cdiv(total, 256), 148 * 8); };
+  int rc = 0;
+  for (int s = first_step; s < first_step + nsteps && !rc; s++) {
+    const int32_t *pairs = outer + (int64_t)s * ntask * 2;
+    for (int t = 0; t < ntask && !rc; t++) {
+      k_pair_gather<<<grid_for(m * w), 256, 0, st>>>(G, ldg, m, pairs, t, bw, A);
+      rc = jh_gram(A, m, m, w, H, st);
+      if (!rc) rc = jh_cholesky(H, w, R, info, st);
+      if (rc) break;
+      k_task_signs<<<1, 256, 0, st>>>(pairs, t, bw, gblock, n_plus, sg);
+      k_inner_wide<<<1, kWideThreads, smem_inner, st>>>(R, Vp, w, inner, sg, tol_c, inner_limit,
+                                                        out, info);
+      k_task_finish<<<1, 32, 0, st>>>(out, info, s, t, trot, counters);
+      rc = jh_gemm(A, m, m, w, Vp, w, w, B, m, st);
+      if (rc) break;
+      k_pair_scatter<<<grid_for(m * w), 256, 0, st>>>(B, m, G, ldg, pairs, t, bw, trot);
+      if (V) {
+        k_pair_gather<<<grid_for(nv * w), 256, 0, st>>>(V, ldv, nv, pairs, t, bw, A);
+        rc = jh_gemm(A, nv, nv, w, Vp, w, w, B, nv, st);
+        if (rc) break;
+        k_pair_scatter<<<grid_for(nv * w), 256, 0, st>>>(B, nv, V, ldv, pairs, t, bw, trot);
+      }
+      g_launches += V ? 8 : 5;
+    }
+  }
+  cudaFreeAsync(scr, st);
+  if (rc) return rc;
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : -(int)e;
 }
 
 // ---------------------------------------------------------------------------
@@ -803,12 +929,17 @@ int jh_block_sweep(double *G, int64_t ldg, int64_t m, int64_t n, double *V, int6
                    const int32_t *inner, int64_t n_plus, int inner_limit, double tol_c,
                    void *workspace, int64_t ws_bytes, unsigned long long *counters,
                    void *stream) {
-  if (w < 2 || w % 2 || w > kMaxW || n % w || m < 1 || ldg < m) return -1000;
+  if (w < 2 || w % 2 || w > 8190 || n % w || m < 1 || ldg < m) return -1000;
   if (V && (nv < 1 || ldv < nv)) return -1000;
   if (first_step < 0 || nsteps < 0 || first_step + nsteps > outer_steps) return -1000;
   if (ws_bytes < ws_bytes_for(n, w, outer_steps)) return -1001;
   if (nsteps == 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
+  if (w > kMaxW) {
+    if (shortening != 0) return -1000;
+    return sweep_wide(G, ldg, m, n, V, ldv, nv, w, outer, gblock, first_step, nsteps, inner,
+                      n_plus, inner_limit, tol_c, workspace, counters, st);
+  }
   if (shortening == 1)
     return sweep_qr(G, ldg, m, n, V, ldv, nv, w, outer, gblock, first_step, nsteps, inner, n_plus,
                     inner_limit, tol_c, workspace, counters, st);

@@ -36,7 +36,8 @@ FULL_BLOCK = "full-block"
 BLOCK_ORIENTED = "block-oriented"
 VARIANTS = (FULL_BLOCK, BLOCK_ORIENTED)
 SHORTENINGS = ("cholesky", "qr")
-MAX_GPU_BLOCK_WIDTH = 64
+# widths above 64 run the general-purpose per-task path (jh_pstep.cu sweep_wide)
+MAX_GPU_BLOCK_WIDTH = 8190
 
 
 class UnsafeScalingError(ValueError):

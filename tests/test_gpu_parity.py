@@ -262,3 +262,31 @@ def test_qr_peeloff_wide_widths_vs_oracle(oracle, m, c, scale):
     rng = np.random.default_rng(m + c)
     a = np.asfortranarray(rng.standard_normal((m, c)) * np.logspace(0, -4, c) * scale)
     assert np.array_equal(J.qr_peeloff(a), oracle.qr_peeloff(a))
+
+
+@pytest.mark.parametrize("n,w,nplus,variant", [(512, 128, 512, "full-block"),
+                                               (768, 96, 400, "full-block"),
+                                               (512, 128, 512, "block-oriented")])
+def test_wide_block_widths_vs_oracle(oracle, n, w, nplus, variant):
+    """Block widths above 64 (the reference takes any even width): the
+    per-task general-purpose path, whole solve bitwise vs the oracle,
+    trig and hyperbolic."""
+    rng = np.random.default_rng(n + w)
+    b = rng.standard_normal((n, n))
+    g = np.asfortranarray(b / np.linalg.norm(b, axis=0) * np.logspace(0, -4, n))
+    kind = "rrow" if (n // (w // 2)) & (n // (w // 2) - 1) == 0 else "mm"
+    ikind = "rrow" if w & (w - 1) == 0 else "mm"
+    cfg = J.SolverConfig(block_width=w, variant=variant, outer_strategy=kind,
+                         inner_strategy=ikind)
+    outer = S.as_table(S.make_strategy(kind, n // (w // 2)))
+    inner = S.as_table(S.make_strategy(ikind, w))
+    try:
+        ref = oracle.block_jacobi(g, nplus, cfg, outer, inner)
+    except oracle.OracleError:
+        with pytest.raises((J.JDefinitenessError, J.RankDeficiencyError)):
+            J.block_jacobi(g, J.Signature(n, nplus), cfg)
+        return
+    res = J.block_jacobi(g, J.Signature(n, nplus), cfg)
+    assert res.stats == ref.stats
+    assert np.array_equal(res.sigma, ref.sigma)
+    assert np.array_equal(res.u, ref.u) and np.array_equal(res.v, ref.v)
