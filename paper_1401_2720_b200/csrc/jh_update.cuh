@@ -83,6 +83,7 @@ __device__ __forceinline__ void update_tma_cta(double *__restrict__ G, int64_t l
     // immediate offsets from per-chunk column pointers
     const int64_t row0 = r0 + cw * (8 * RB) + g;
     double *cp = pout + row0, *cq = qout + row0;
+    const int64_t left = s1 - row0;  // rows of this warp's part still in the slab
 #pragma unroll
     for (int rb = 0; rb < RB; rb++) {
       const int rl = cw * (8 * RB) + rb * 8;
@@ -96,7 +97,7 @@ __device__ __forceinline__ void update_tma_cta(double *__restrict__ G, int64_t l
       for (int kk = 0; kk < NK; kk++)
 #pragma unroll
         for (int Y = 0; Y < NT; Y++) dmma(acc[Y][0], acc[Y][1], a[kk], bf[kk][Y]);
-      if (row0 + rb * 8 < s1) {
+      if (rb * 8 < left) {
 #pragma unroll
         for (int Y = 0; Y < NT; Y++)
 #pragma unroll

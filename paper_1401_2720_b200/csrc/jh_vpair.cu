@@ -109,46 +109,60 @@ struct VpArgs {
 // cb1 + k - 16 (k >= 16) times V' (fragments in registers); each result
 // entry goes to the slot in place when keep[block] and to HBM when
 // fin[block] (block = slot block of its column, 0..3)
-__device__ __forceinline__ void vp_transform(double *buf, int cb0, int cb1,
-                                             const double (&bf)[8][4], unsigned keep,
-                                             unsigned fin, double *V, int64_t ldv,
-                                             const int64_t (&gcol)[4], int64_t r, int nr, int g,
-                                             int t) {
-  // Lanes with t >= 2 (sw = 1) store their two values in the opposite order
-  // (conflict-free 64-bit shared stores).  Their V' fragments carry the
-  // tile's columns 4 <-> 5 and 6 <-> 7 swapped (vp_load_bfrag), so the
-  // accumulator acc[j] already holds column 2t + (j ^ sw): no value select.
-  const int sw = (t >> 1) & 1;
-  // per-call addressing, hoisted out of the row loop: the shared-memory
-  // column offsets of the 8 A fragments, and per output tile and value the
-  // slot column and the global column pointer at row g
+// Addressing of one transform within a V item, set up once per item (it
+// does not change from chunk to chunk): the shared-memory offsets of the 8
+// A fragments, and per output tile Y the slot column and the global column
+// pointer of value 0 at row g (value 1 sits 1 - 2 sw columns away), and
+// whether the tile's block stays in the slot (keep) or goes to HBM (fin).
+//
+// Lanes with t >= 2 (sw = 1) store their two values in the opposite order
+// (conflict-free 64-bit shared stores).  Their V' fragments carry the tile's
+// columns 4 <-> 5 and 6 <-> 7 swapped (vp_load_bfrag), so the accumulator
+// acc[j] already holds column 2t + (j ^ sw): no value select.
+struct VpAddr {
   int aoff[8];
+  int soff[4];
+  const double *gp[4];  // at row r0 + g of the item's slab
+  int dsj;
+  int64_t dgj;
+  bool kp[4], tg[4];
+};
+
+__device__ __forceinline__ VpAddr vp_addr(int cb0, int cb1, unsigned keep, unsigned fin,
+                                          const double *V, int64_t ldv, const int64_t (&gcol)[4],
+                                          int64_t r0, int g, int t) {
+  VpAddr d;
+  const int sw = (t >> 1) & 1;
 #pragma unroll
   for (int kk = 0; kk < 8; kk++)
-    aoff[kk] = ((kk < 4 ? cb0 + 4 * kk : cb1 + 4 * kk - 16) + t) * kVLd + g;
-  // (value j = 1 sits in the column of value 0 plus 1 - 2 sw)
-  int soff[4];
-  double *gp[4];
-  bool kp[4], tg[4];
-  const int dsj = (1 - 2 * sw) * kVLd;
-  const int64_t dgj = (1 - 2 * sw) * ldv;
+    d.aoff[kk] = ((kk < 4 ? cb0 + 4 * kk : cb1 + 4 * kk - 16) + t) * kVLd + g;
+  d.dsj = (1 - 2 * sw) * kVLd;
+  d.dgj = (1 - 2 * sw) * ldv;
 #pragma unroll
   for (int Y = 0; Y < 4; Y++) {
     const int cbase = Y < 2 ? cb0 : cb1, blk = cbase >> 4;
-    kp[Y] = (keep >> blk) & 1;
-    tg[Y] = (fin >> blk) & 1;
+    d.kp[Y] = (keep >> blk) & 1;
+    d.tg[Y] = (fin >> blk) & 1;
     const int64_t gc = blk == 0 ? gcol[0] : blk == 1 ? gcol[1] : blk == 2 ? gcol[2] : gcol[3];
     const int n = 8 * (Y & 1) + 2 * t + sw;
-    soff[Y] = (cbase + n) * kVLd + g;
-    gp[Y] = V + (gc + n) * ldv + r + g;
+    d.soff[Y] = (cbase + n) * kVLd + g;
+    d.gp[Y] = V + (gc + n) * ldv + r0 + g;
   }
+  return d;
+}
+
+// rows 0..kVRch-1 of a staged chunk (rows dr.. of the slab) times V'
+// (fragments in registers); each result goes to the slot in place (kp) and
+// / or to HBM (tg)
+__device__ __forceinline__ void vp_transform(double *buf, const double (&bf)[8][4],
+                                             const VpAddr &d, int64_t dr, int nr, int g) {
 #pragma unroll 1
   for (int rb = 0; rb < kVRch / 8; rb += 2) {
     double a[2][8];
 #pragma unroll
     for (int h = 0; h < 2; h++)
 #pragma unroll
-      for (int kk = 0; kk < 8; kk++) a[h][kk] = buf[aoff[kk] + 8 * (rb + h)];
+      for (int kk = 0; kk < 8; kk++) a[h][kk] = buf[d.aoff[kk] + 8 * (rb + h)];
     double acc[2][4][2];
 #pragma unroll
     for (int h = 0; h < 2; h++)
@@ -161,6 +175,7 @@ __device__ __forceinline__ void vp_transform(double *buf, int cb0, int cb1,
 #pragma unroll
         for (int Y = 0; Y < 4; Y++) dmma(acc[h][Y][0], acc[h][Y][1], a[h][kk], bf[kk][Y]);
     const int ro = 8 * rb;
+    const int64_t go = dr + ro;
 #pragma unroll
     for (int h = 0; h < 2; h++) {
       const bool in = ro + 8 * h + g < nr;
@@ -168,8 +183,9 @@ __device__ __forceinline__ void vp_transform(double *buf, int cb0, int cb1,
       for (int Y = 0; Y < 4; Y++) {
 #pragma unroll
         for (int j = 0; j < 2; j++) {
-          if (kp[Y]) buf[soff[Y] + (j ? dsj : 0) + ro + 8 * h] = acc[h][Y][j];
-          if (tg[Y] && in) st_f64(gp[Y] + (j ? dgj : 0) + ro + 8 * h, acc[h][Y][j]);
+          if (d.kp[Y]) buf[d.soff[Y] + (j ? d.dsj : 0) + ro + 8 * h] = acc[h][Y][j];
+          if (d.tg[Y] && in)
+            st_f64(const_cast<double *>(d.gp[Y]) + (j ? d.dgj : 0) + go + 8 * h, acc[h][Y][j]);
         }
       }
     }
@@ -254,14 +270,15 @@ __device__ __forceinline__ void vpair_cta(const VpArgs &a, int c, int k, VpSmem 
   const int cb1 = phaseA ? 32 * h + 16 : 16 * ib[h][1];
   const unsigned keep = phaseA ? touchedB : 0u;
   const unsigned fin = phaseA ? (0xFu & ~touchedB) : 0xFu;
+  const VpAddr d = vp_addr(cb0, cb1, keep, fin, a.V, a.ldv, gcol, r0, g, t);
   for (int cc = 0; cc < nchunk; cc++) {
     const int st = cc % kVStages;
     const uint32_t par = (uint32_t)((cc / kVStages) & 1);
     mbar_wait(phaseA ? &S.full[st] : &S.adone[st], par);
     double *buf = &S.ring[st][0][0];
-    const int64_t r = r0 + (int64_t)cc * kVRch;
-    const int nr = (int)min64(kVRch, r1 - r);
-    if (mine) vp_transform(buf, cb0, cb1, bf, keep, fin, a.V, a.ldv, gcol, r, nr, g, t);
+    const int64_t dr = (int64_t)cc * kVRch;
+    const int nr = (int)min64(kVRch, r1 - r0 - dr);
+    if (mine) vp_transform(buf, bf, d, dr, nr, g);
     if (phaseA && mine && keep) fence_async_smem_cta();  // before the slot's next TMA fill
     __syncwarp();
     if (lane == 0) mbar_arrive(phaseA ? &S.adone[st] : &S.empty[st]);
