@@ -14,6 +14,8 @@
 //   C/D (8 x 8)     : lane holds D[g][2t], D[g][2t + 1]
 #pragma once
 
+#include <cuda.h>
+
 #include "jh_common.cuh"
 
 namespace jh {
@@ -82,6 +84,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       "@!P bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
+      : "memory");
+}
+
+// TMA tensor tile load: the box at (row, col) of the 2-D tensor map into
+// shared memory (128 B aligned), completion on `bar` as transaction bytes
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int row, int col,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(smem_u32(dst)), "l"((uint64_t)map), "r"(row), "r"(col), "r"(smem_u32(bar))
       : "memory");
 }
 

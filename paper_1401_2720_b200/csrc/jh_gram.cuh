@@ -23,10 +23,10 @@ struct GramTiles {
   static constexpr int MY = (NTILE + NW - 1) / NW;
 };
 
-template <int W, int NW, int WARP, int RCH = kRch>
+template <int W, int NW, int WARP, int RCH = kRch, int LD = RCH + 4>
 __device__ __forceinline__ void gram_chunk(const double *buf, int nr, double (&acc)[GramTiles<W, NW>::MY][2],
                                            int t) {
-  constexpr int NT = W / 8, LD = RCH + 4;
+  constexpr int NT = W / 8;
   auto tiles = [&](const double (&f)[NT]) {
     int i = 0, mine = 0;
 #pragma unroll
@@ -48,20 +48,24 @@ __device__ __forceinline__ void gram_chunk(const double *buf, int nr, double (&a
   if (nr == RCH) {
     // explicit two-stage register pipeline: fragments of k-step kk+1 are
     // loaded before the DMMAs of k-step kk are issued
+    // (an odd k-step count -- RCH = 4 mod 16 for the dense tensor-tile
+    // stages -- ends with one k-step in fa)
+    constexpr int NKS = RCH / 4;
     double fa[NT], fb[NT];
 #pragma unroll
     for (int X = 0; X < NT; X++) fa[X] = buf[X * 8 * LD];
 #pragma unroll
-    for (int kk = 0; kk < RCH / 4; kk += 2) {
+    for (int kk = 0; kk + 1 < NKS; kk += 2) {
 #pragma unroll
       for (int X = 0; X < NT; X++) fb[X] = buf[X * 8 * LD + 4 * (kk + 1)];
       tiles(fa);
-      if (kk + 2 < RCH / 4) {
+      if (kk + 2 < NKS) {
 #pragma unroll
         for (int X = 0; X < NT; X++) fa[X] = buf[X * 8 * LD + 4 * (kk + 2)];
       }
       tiles(fb);
     }
+    if constexpr (NKS % 2) tiles(fa);
   } else {
     const int nks = (nr + 3) / 4;
     for (int kk = 0; kk < nks; kk++) step(kk, true);

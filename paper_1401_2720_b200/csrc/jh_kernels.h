@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace jh {
@@ -16,6 +17,12 @@ void ensure_smem(const void *fn, int bytes);
 int sm_count();       // SMs of the current device
 // per-kernel-class CUDA event timing (jh_profile_begin / _end)
 void prof_mark(cudaStream_t st, int cls, bool after);
+// TMA tensor map of a column-major FP64 matrix (rows x cols, leading
+// dimension ld, 16-byte aligned columns) with boxes of box_rows x box_cols;
+// rows past the end read as zeros.  false if the driver entry point is
+// unavailable or the shape is not encodable.
+bool make_col_tmap(CUtensorMap *map, const double *A, int64_t rows, int64_t cols, int64_t ld,
+                   int box_rows, int box_cols);
 
 // ---- DMMA/TMA Gram of every task of a p-step (jh_tiles.cu); w in {16, 32}.
 bool gram_tma_ok(int w, int64_t m, int64_t ldg);

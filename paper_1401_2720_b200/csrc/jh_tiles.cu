@@ -35,14 +35,14 @@ namespace jh {
 // i == vw (mod NW * SPLIT).  SPLIT > 1 spreads one task's tile chains over
 // several SMs (few tasks per p-step: the sharded solve), each CTA streaming
 // the whole pair (the second read of a chunk is an L2 hit).
-template <int W, int VW, int RCH>
+template <int W, int VW, int RCH, int LD>
 __device__ __forceinline__ void gram_chunk_dispatch(int vw, const double *buf, int nr,
                                                     double (&acc)[GramTiles<W, VW>::MY][2],
                                                     int t) {
   switch (vw) {
 #define JH_GC(k) \
   case k:        \
-    if constexpr (k < VW) gram_chunk<W, VW, (k < VW ? k : 0), RCH>(buf, nr, acc, t); \
+    if constexpr (k < VW) gram_chunk<W, VW, (k < VW ? k : 0), RCH, LD>(buf, nr, acc, t); \
     break;
     JH_GC(0) JH_GC(1) JH_GC(2) JH_GC(3) JH_GC(4) JH_GC(5) JH_GC(6) JH_GC(7) JH_GC(8) JH_GC(9)
 #undef JH_GC
@@ -65,12 +65,19 @@ __device__ __forceinline__ void gram_store_dispatch(int vw, double *H,
   }
 }
 
+// The producer loads each chunk as two TMA tensor tiles (rows x W/2 columns
+// of block p and of block q, `tmap` over G) into a dense [W][kGramRch]
+// stage; kGramRch = 4 (mod 16) keeps the fragment loads conflict free.
+// Rows past m arrive as zeros (the consumers stop at m anyway).  Without a
+// tensor map (use_tmap false) one bulk copy per column, padded stride.
 template <int W, int NW, int kGramRch, int kGramStages, int SPLIT = 1>
 __global__ void __launch_bounds__(32 * (NW + 1))
 k_gram_tma(const double *__restrict__ G, int64_t ldg, int64_t m,
-           const int32_t *__restrict__ pairs, double *__restrict__ Hbuf) {
-  // warp 0 produces (TMA bulk copies), warps 1..NW consume (DMMA)
-  constexpr int BW = W / 2, VW = NW * SPLIT, MY = GramTiles<W, VW>::MY, kGramLd = kGramRch + 4;
+           const int32_t *__restrict__ pairs, double *__restrict__ Hbuf,
+           const __grid_constant__ CUtensorMap tmap, bool use_tmap) {
+  // warp 0 produces (TMA), warps 1..NW consume (DMMA)
+  static_assert(kGramRch % 16 == 4, "dense tensor-tile stage: column stride 4 (mod 16)");
+  constexpr int BW = W / 2, VW = NW * SPLIT, MY = GramTiles<W, VW>::MY, kGramLd = kGramRch;
   static_assert(VW <= 10, "at most one virtual warp per tile of w = 32");
   extern __shared__ __align__(128) double sm[];  // [kGramStages][W][kGramLd]
   __shared__ __align__(8) uint64_t full[kGramStages], empty[kGramStages];
@@ -92,6 +99,14 @@ k_gram_tma(const double *__restrict__ G, int64_t ldg, int64_t m,
       const int s = (int)(c % kGramStages);
       if (c >= kGramStages) mbar_wait(&empty[s], (uint32_t)(((c / kGramStages) - 1) & 1));
       const int64_t r0 = c * kGramRch;
+      if (use_tmap) {
+        if (lane == 0) {
+          mbar_expect_tx(&full[s], (uint32_t)(W * kGramRch * 8));  // whole boxes
+          tma_load_2d(sm + (size_t)s * W * kGramLd, &tmap, (int)r0, p * BW, &full[s]);
+          tma_load_2d(sm + ((size_t)s * W + BW) * kGramLd, &tmap, (int)r0, q * BW, &full[s]);
+        }
+        continue;
+      }
       const uint32_t bytes = (uint32_t)min64(kGramRch, m - r0) * 8u;
       if (lane == 0) mbar_expect_tx(&full[s], bytes * W);
       __syncwarp();
@@ -112,7 +127,7 @@ k_gram_tma(const double *__restrict__ G, int64_t ldg, int64_t m,
     mbar_wait(&full[s], (uint32_t)((c / kGramStages) & 1));
     const double *buf = sm + (size_t)s * W * kGramLd + (size_t)g * kGramLd + t;
     const int nr = (int)min64(kGramRch, m - c * kGramRch);
-    gram_chunk_dispatch<W, VW, kGramRch>(vw, buf, nr, acc, t);
+    gram_chunk_dispatch<W, VW, kGramRch, kGramLd>(vw, buf, nr, acc, t);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
@@ -289,10 +304,13 @@ bool gram_tma_ok(int w, int64_t m, int64_t ldg) {
 template <int W, int NW, int RCH, int STG, int SPLIT = 1>
 static void launch_gram_nw(const double *G, int64_t ldg, int64_t m, const int32_t *pairs,
                            int ntask, double *Hbuf, cudaStream_t st) {
-  const size_t smem = sizeof(double) * (size_t)STG * W * (RCH + 4);
+  const size_t smem = sizeof(double) * (size_t)STG * W * RCH;
   ensure_smem((const void *)k_gram_tma<W, NW, RCH, STG, SPLIT>, (int)smem);
-  k_gram_tma<W, NW, RCH, STG, SPLIT><<<ntask * SPLIT, 32 * (NW + 1), smem, st>>>(G, ldg, m,
-                                                                               pairs, Hbuf);
+  // the table's block-columns span ntask * W columns of G
+  CUtensorMap tmap;
+  const bool ok = make_col_tmap(&tmap, G, m, (int64_t)ntask * W, ldg, RCH, W / 2);
+  k_gram_tma<W, NW, RCH, STG, SPLIT><<<ntask * SPLIT, 32 * (NW + 1), smem, st>>>(
+      G, ldg, m, pairs, Hbuf, tmap, ok);
 }
 
 // Ring shape by the CTAs an SM must hold for one wave: longer chunks (one
@@ -305,11 +323,11 @@ static void launch_gram_shape(const double *G, int64_t ldg, int64_t m, const int
                               int ntask, int sms, double *Hbuf, cudaStream_t st) {
   const int per_sm = (ntask + sms - 1) / sms;
   if (per_sm <= 2)
-    launch_gram_nw<W, NW, 192, 2>(G, ldg, m, pairs, ntask, Hbuf, st);
+    launch_gram_nw<W, NW, 196, 2>(G, ldg, m, pairs, ntask, Hbuf, st);
   else if (per_sm == 3)
-    launch_gram_nw<W, NW, 128, 2>(G, ldg, m, pairs, ntask, Hbuf, st);
+    launch_gram_nw<W, NW, 132, 2>(G, ldg, m, pairs, ntask, Hbuf, st);
   else
-    launch_gram_nw<W, NW, 104, 2>(G, ldg, m, pairs, ntask, Hbuf, st);
+    launch_gram_nw<W, NW, 100, 2>(G, ldg, m, pairs, ntask, Hbuf, st);
 }
 
 template <int W>
@@ -329,11 +347,11 @@ static void launch_gram_t(const double *G, int64_t ldg, int64_t m, const int32_t
   const int sms = sm_count();
   if constexpr (W == 32) {
     if (ntask <= sms / JH_GS2_DIV) {
-      launch_gram_nw<W, 5, 192, 2, 2>(G, ldg, m, pairs, ntask, Hbuf, st);
+      launch_gram_nw<W, 5, 196, 2, 2>(G, ldg, m, pairs, ntask, Hbuf, st);
       return;
     }
     if (ntask <= sms * JH_G10_MUL) {
-      launch_gram_nw<W, 10, 192, 2, 1>(G, ldg, m, pairs, ntask, Hbuf, st);
+      launch_gram_nw<W, 10, 196, 2, 1>(G, ldg, m, pairs, ntask, Hbuf, st);
       return;
     }
   }
@@ -350,7 +368,7 @@ void launch_gram_tma(const double *G, int64_t ldg, int64_t m, const int32_t *pai
   else if (w == 32)
     launch_gram_t<32>(G, ldg, m, pairs, ntask, Hbuf, st);
   else  // w = 64: 36 lower tiles over 4 consumer warps (9 chains each), 3 x 64-row ring (104 KB)
-    launch_gram_nw<64, 4, 64, 3>(G, ldg, m, pairs, ntask, Hbuf, st);
+    launch_gram_nw<64, 4, 68, 3>(G, ldg, m, pairs, ntask, Hbuf, st);
 }
 
 bool update_dmma_ok(int w) { return w == 16 || w == 32 || w == 64; }
