@@ -8,7 +8,7 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
 LIB = ROOT / "paper_1401_2720_b200" / "_lib" / "libjhsvd_b200.so"
-OPS = ("DMMA", "UBLKCP", "DFMA", "LDGSTS", "SYNCS", "MUFU")
+OPS = ("DMMA", "UTMALDG", "UBLKCP", "DFMA", "LDGSTS", "SYNCS", "MUFU")
 
 
 def main():
@@ -38,14 +38,15 @@ def main():
     print("`cuobjdump -sass paper_1401_2720_b200/_lib/libjhsvd_b200.so`, counted per kernel "
           "(static instructions; tools/sass_summary.py).")
     print("DMMA = `mma.sync.m8n8k4.f64` (FP64 tensor core), UBLKCP = `cp.async.bulk` (TMA engine "
-          "bulk copy), LDGSTS = `cp.async`, SYNCS = mbarrier operations, MUFU = FP64 reciprocal / "
+          "bulk copy), UTMALDG = `cp.async.bulk.tensor` (TMA tensor tile), LDGSTS = `cp.async`, SYNCS = mbarrier operations, MUFU = FP64 reciprocal / "
           "rsqrt seeds of the IEEE division / sqrt paths.\n")
-    print("| DMMA | UBLKCP | DFMA | LDGSTS | SYNCS | MUFU64 | kernel |")
-    print("|---|---|---|---|---|---|---|")
+    print("| DMMA | UTMALDG | UBLKCP | DFMA | LDGSTS | SYNCS | MUFU64 | kernel |")
+    print("|---|---|---|---|---|---|---|---|")
     rows = sorted(zip(demangled, counts.values()), key=lambda r: -r[1]["DMMA"])
     for dn, c in rows:
         dn = re.sub(r"\(.*", "", dn.replace("(anonymous namespace)::", ""))
-        print(f"| {c['DMMA']} | {c['UBLKCP']} | {c['DFMA']} | {c['LDGSTS']} | {c['SYNCS']} | "
+        print(f"| {c['DMMA']} | {c['UTMALDG']} | {c['UBLKCP']} | {c['DFMA']} | {c['LDGSTS']} | "
+              f"{c['SYNCS']} | "
               f"{c['MUFU']} | `{dn}` |")
 
 
