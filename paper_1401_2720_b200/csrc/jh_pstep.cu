@@ -794,11 +794,8 @@ static int sweep_vpaired(double *G, int64_t ldg, int64_t m, int64_t n, double *V
   // (16384^2: 1.83 vs 1.80) and with fewer tasks than SMs, where the split
   // Gram kernel is faster (profiles/r02/README.md)
   const int sms = sm_count();
-#ifndef JH_GMIX_FORCE
-#define JH_GMIX_FORCE 0
-#endif
   const bool gmix = w == 32 && nsteps > 1 &&
-                    (JH_GMIX_FORCE || (m <= 8192 && m * n <= (int64_t(1) << 26)) ||
+                    ((m <= 8192 && m * n <= (int64_t(1) << 26)) ||
                      (ntask > sms && ntask <= 2 * sms && m <= 16384));
   if (gmix) {
     cudaMemsetAsync(gcnt, 0, sizeof(int64_t) * ntask, st);
