@@ -38,19 +38,24 @@ def main():
         e_start = pynvml.nvmlDeviceGetTotalEnergyConsumption(h)
         ms, stats = [], []
         eng.tasks_rotated = []
+        joules_sweep = []
         for _ in range(eng.cfg.max_block_sweeps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            j0 = pynvml.nvmlDeviceGetTotalEnergyConsumption(h)
             e0.record()
             rot, proper = eng.one_sweep(G, V)
             e1.record()
             torch.cuda.synchronize()
+            joules_sweep.append(round((pynvml.nvmlDeviceGetTotalEnergyConsumption(h) - j0) / 1e3, 1))
             ms.append(round(e0.elapsed_time(e1), 1))
             stats.append((rot, proper))
             if proper == 0:
                 break
         joules = (pynvml.nvmlDeviceGetTotalEnergyConsumption(h) - e_start) / 1e3
         print(json.dumps({"engine": e, "total_s": round(sum(ms) / 1e3, 3), "joules": joules,
-                          "ms_per_sweep": ms, "sweeps": len(ms)}), flush=True)
+                          "ms_per_sweep": ms, "joules_per_sweep": joules_sweep,
+                          "tasks_rotated": list(eng.tasks_rotated), "sweeps": len(ms)}),
+              flush=True)
         del G, V
     eng.engine = default
 
