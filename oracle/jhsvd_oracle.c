@@ -519,16 +519,22 @@ void or_inner_jacobi(double *r, double *v, int c, const int32_t *steps, int nste
     out[0] = total_rot; out[1] = total_proper; out[2] = sweeps; out[3] = 0; out[4] = -1;
 }
 
-/* out = a @ vacc, per-entry fma chain over ascending k (blockkernel.py:407-417) */
+/* out = a @ vacc, per-entry fma chain over ascending k (blockkernel.py:407-417).
+ * Rows are processed in cache-sized blocks (tall pairs: a 131072-row column
+ * is 1 MB); every entry's chain still runs over k = 0..c-1 in order. */
+#define POST_CHUNK_ 2048
 void or_postmultiply(const double *a, int64_t lda, int64_t m, int c, const double *vacc,
                      double *out, int64_t ldo) {
-    for (int j = 0; j < c; j++) {
-        double *o = out + (int64_t)j * ldo;
-        for (int64_t i = 0; i < m; i++) o[i] = 0.0;
-        for (int k = 0; k < c; k++) {
-            double w = vacc[(int64_t)j * c + k];
-            const double *ak = a + (int64_t)k * lda;
-            for (int64_t i = 0; i < m; i++) o[i] = fma(ak[i], w, o[i]);
+    for (int64_t r0 = 0; r0 < m; r0 += POST_CHUNK_) {
+        const int64_t r1 = r0 + POST_CHUNK_ < m ? r0 + POST_CHUNK_ : m;
+        for (int j = 0; j < c; j++) {
+            double *o = out + (int64_t)j * ldo;
+            for (int64_t i = r0; i < r1; i++) o[i] = 0.0;
+            for (int k = 0; k < c; k++) {
+                double w = vacc[(int64_t)j * c + k];
+                const double *ak = a + (int64_t)k * lda;
+                for (int64_t i = r0; i < r1; i++) o[i] = fma(ak[i], w, o[i]);
+            }
         }
     }
 }
