@@ -8,8 +8,9 @@
   tests/golden/offline/config4.json.
 * config 2 (4096^2 column-graded, kappa = 1e12, block-oriented): the whole
   solve against the C oracle run here on the host cores.
-* config 5 (131072 x 8192): the first p-steps of sweep 1, G and V bitwise
-  against the oracle on the same input.
+* config 5 (131072 x 8192): the same against tests/golden/offline/config5.json,
+  and the first p-steps of sweep 1, G and V bitwise against the oracle run
+  in the test.
 * hybrid early stop of the three-level outer level with the product kernels
   against the same rule on oracle workers.
 The C oracle (oracle/) is the checker; the product path never calls it.
@@ -42,7 +43,7 @@ def _offline(name):
     return json.loads(p.read_text())
 
 
-@pytest.mark.parametrize("name", ["config3", "config4"])
+@pytest.mark.parametrize("name", ["config3", "config4", "config5"])
 def test_whole_solve_bitwise_vs_offline_oracle(name):
     import torch
 
