@@ -24,6 +24,10 @@ Prints ONE JSON line (rank 0).  Besides the contract keys it carries
    host<->device copies inside the timed region;
  - roofline: the dominant kernel's algorithmic HBM bytes / CUDA-event time;
  - fp64_roofline: the whole solve's DMMA flops against the measured DMMA rate;
+ - energy_roofline: the solve runs at the board power limit, so joules bound
+   its speed: NVML energy over the timed region against the floor DMMA
+   flops x pJ/flop + HBM bytes x pJ/byte + idle power x time
+   (profiles/r02/energy_probe.json); clocks carries power draw and limit;
  - cpu_baseline: the C oracle (a port of the reference CPU solver) timed on
    a bounded prefix of the same solve on this host, extrapolated with the
    per-sweep cost profile of the oracle's own offline whole solve;
